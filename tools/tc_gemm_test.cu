@@ -1,0 +1,106 @@
+// Standalone check of the tcgen05 GEMM (tc_gemm.cuh) against a CPU fp64 dot
+// product on sampled entries, plus a timing line per shape.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2212_01543_b200/csrc \
+//        tools/tc_gemm_test.cu -o tools/tc_gemm_test
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+#include <random>
+#include "tc_gemm.cuh"
+#include "tmap.h"
+
+using namespace hrt;
+
+struct StoreEpi {
+  float* C;
+  int ldc;
+  struct State {};
+  __device__ void begin(State&, int, int) const {}
+  __device__ void chunk(State&, int row, int col0, const float* v, int n) const {
+    for (int i = 0; i < n; ++i) C[(size_t)row * ldc + col0 + i] = v[i];
+  }
+  __device__ void end(State&, int, int) const {}
+};
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+template <int BN, int ST>
+bool run(int M, int N, int K) {
+  std::mt19937 g(M * 7 + N * 3 + K);
+  std::normal_distribution<float> nd(0.f, 1.f);
+  std::vector<__nv_bfloat16> hA((size_t)M * K), hB((size_t)N * K);
+  for (auto& x : hA) x = __float2bfloat16(nd(g));
+  for (auto& x : hB) x = __float2bfloat16(nd(g));
+  __nv_bfloat16 *dA, *dB;
+  float* dC;
+  CK(cudaMalloc(&dA, hA.size() * 2));
+  CK(cudaMalloc(&dB, hB.size() * 2));
+  CK(cudaMalloc(&dC, (size_t)M * N * 4));
+  CK(cudaMemcpy(dA, hA.data(), hA.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, hB.data(), hB.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dC, 0xff, (size_t)M * N * 4));
+  CUtensorMap ta = make_tmap_bf16_kmajor(dA, M, K, K, TC_BM);
+  CUtensorMap tb = make_tmap_bf16_kmajor(dB, N, K, K, BN);
+  auto kern = tc_gemm_kernel<BN, ST, StoreEpi>;
+  int smem = TcSmem<BN, ST>::TOTAL;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((N + BN - 1) / BN, (M + TC_BM - 1) / TC_BM);
+  StoreEpi epi{dC, N};
+  kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<float> hC((size_t)M * N);
+  CK(cudaMemcpy(hC.data(), dC, hC.size() * 4, cudaMemcpyDeviceToHost));
+  double maxerr = 0;
+  int bad = 0;
+  std::uniform_int_distribution<int> um(0, M - 1), un(0, N - 1);
+  for (int s = 0; s < 4000; ++s) {
+    int i = s < 64 ? (s % M) : um(g), j = s < 64 ? ((s * 37) % N) : un(g);
+    double ref = 0;
+    for (int k = 0; k < K; ++k)
+      ref += (double)__bfloat162float(hA[(size_t)i * K + k]) * (double)__bfloat162float(hB[(size_t)j * K + k]);
+    double err = fabs(ref - hC[(size_t)i * N + j]) / (1.0 + fabs(ref));
+    if (err > maxerr) maxerr = err;
+    if (err > 1e-3) {
+      if (bad < 5) printf("   mismatch C[%d,%d] = %f ref %f\n", i, j, hC[(size_t)i * N + j], ref);
+      ++bad;
+    }
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int w = 0; w < 3; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  cudaEventRecord(e0);
+  const int iters = 20;
+  for (int w = 0; w < iters; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  double us = ms * 1000.0 / iters;
+  double tflops = 2.0 * M * N * K / (us * 1e-6) / 1e12;
+  double gbs = ((double)M * K * 2 + (double)N * K * 2 + (double)M * N * 4) / (us * 1e-6) / 1e9;
+  printf("BN=%3d ST=%d M=%6d N=%6d K=%5d : maxrel=%.2e bad=%d  %.2f us  %.1f TFLOP/s  %.0f GB/s  %s\n", BN, ST, M,
+         N, K, maxerr, bad, us, tflops, gbs, bad ? "FAIL" : "ok");
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  return bad == 0;
+}
+
+int main() {
+  bool ok = true;
+  ok &= run<256, 4>(1, 256, 64);
+  ok &= run<256, 4>(1, 32000, 512);
+  ok &= run<256, 4>(200, 512, 512);
+  ok &= run<256, 4>(1000, 1536, 512);
+  ok &= run<128, 6>(300, 2048, 512);
+  ok &= run<64, 8>(64, 512, 2048);
+  ok &= run<256, 4>(1024, 32000, 512);
+  ok &= run<256, 4>(8192, 2048, 512);
+  ok &= run<256, 4>(8192, 512, 2048);
+  ok &= run<128, 6>(8192, 512, 2048);
+  printf(ok ? "ALL OK\n" : "SOME FAILED\n");
+  return ok ? 0 : 1;
+}
