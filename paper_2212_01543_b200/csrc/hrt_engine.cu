@@ -1,0 +1,1424 @@
+// B200-native HRT inference engine: weights, device arena, the three phases
+// (encoder, Stage-I skip-AT, Stage-II fill), and the C ABI of include/hrt_b200.h.
+//
+// Reference path (/root/reference/pkg/src/hrt): infer.py (session), decoding.py
+// (search/selection), arena.py (buffer reuse), kernels.py (LN/softmax).
+// Batched execution reproduces per-sentence results: sentences are packed
+// ("varlen") so no padded key is ever attended; Stage-I rows of different
+// sentences are independent; Stage-II candidates own disjoint row slots.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hrt_b200.h"
+#include "common.cuh"
+#include "gemm_epi.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+#include "tmap.h"
+
+namespace hrt {
+
+struct HrtError : std::runtime_error {
+  hrt_status code;
+  HrtError(hrt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(x)                                                                                     \
+  do {                                                                                                 \
+    cudaError_t _e = (x);                                                                              \
+    if (_e != cudaSuccess)                                                                             \
+      throw HrtError(HRT_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " @" + \
+                                       std::to_string(__LINE__));                                      \
+  } while (0)
+
+static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+static inline size_t align_up(size_t n, size_t a = 256) { return (n + a - 1) / a * a; }
+
+enum KClass { K_GEMM = 1, K_VOCAB = 2, K_ATTN = 4, K_OTHER = 8 };
+
+// ---------------------------------------------------------------------------
+// Device arena: one allocation, per-phase buffer plans carved at fixed
+// offsets; phases alias each other (reference arena.py:23-51; LightSeq-style
+// reuse). Sized once in closed form from the engine capacity.
+// ---------------------------------------------------------------------------
+struct Plan {
+  size_t off = 0;
+  template <typename X>
+  X* take(char* base, size_t count) {
+    size_t o = off;
+    off = align_up(off + count * sizeof(X));
+    return base ? reinterpret_cast<X*>(base + o) : nullptr;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// engine
+// ---------------------------------------------------------------------------
+struct EngineBase {
+  hrt_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  hrt_stats stats{};
+  // kernel-class timing
+  int timed_class = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  double t_bytes = 0, t_flops = 0;
+  int64_t t_launches = 0;
+
+  virtual ~EngineBase() {
+    for (auto& p : ev_pool) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    if (stream) cudaStreamDestroy(stream);
+  }
+  virtual void encode(const int32_t* ids, const int32_t* lens, int n, float* mem_out) = 0;
+  virtual void start_cache(int rows, int cap, const int32_t* row_seq) = 0;
+  virtual void step(const int32_t* tokens, int position, float* logp_out) = 0;
+  virtual void reorder(const int32_t* parents) = 0;
+  virtual void parallel_logits(const int32_t* ids, const int32_t* pos, const uint8_t* pad, int B, int T, int mode,
+                               const int32_t* seq, float* logits_out) = 0;
+  virtual void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) = 0;
+  virtual void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
+                         const int32_t* caps, const hrt_translate_out* out, int on_device) = 0;
+
+  // --- launch bookkeeping -------------------------------------------------
+  struct Scope {
+    EngineBase* e;
+    std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+    Scope(EngineBase* eng, int cls, double bytes, double flops) : e(eng) {
+      if (e->timed_class & cls) {
+        if (e->ev_used == e->ev_pool.size()) {
+          cudaEvent_t a, b;
+          cudaEventCreate(&a);
+          cudaEventCreate(&b);
+          e->ev_pool.emplace_back(a, b);
+        }
+        ev = &e->ev_pool[e->ev_used++];
+        cudaEventRecord(ev->first, e->stream);
+        e->t_bytes += bytes;
+        e->t_flops += flops;
+        e->t_launches += 1;
+      }
+    }
+    ~Scope() {
+      if (ev) cudaEventRecord(ev->second, e->stream);
+      e->stats.kernel_launches += 1;
+    }
+  };
+  void check_launch() {
+    cudaError_t er = cudaGetLastError();
+    if (er != cudaSuccess) throw HrtError(HRT_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(er));
+  }
+};
+
+template <typename T>
+struct Engine : EngineBase {
+  static constexpr bool BF16 = std::is_same<T, bf16>::value;
+  int d, ff, H, dh, Le, Ld, V, Lmax, P;  // P = PE rows
+  float emb_scale, att_scale;
+
+  // ---- weights ----
+  struct EncW {
+    T *wqkv, *wo, *w1, *w2;
+    float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
+  };
+  struct DecW {
+    T *wqkv, *wo, *wqc, *woc, *w1, *w2;
+    float *bqkv, *bo, *bqc, *boc, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b, *ln3g, *ln3b;
+  };
+  std::vector<EncW> enc;
+  std::vector<DecW> dec;
+  T *E = nullptr, *wxkv = nullptr;
+  float *bxkv = nullptr, *pe = nullptr, *enc_lng, *enc_lnb, *dec_lng, *dec_lnb;
+  char* wblob = nullptr;
+  char* vblob = nullptr;
+
+  // ---- capacity ----
+  int Bmax, beam_max, Me_max, R_max, cap_max, M2_max, Mm_max, nt_max, logit_rows;
+
+  // ---- persistent device buffers ----
+  char* persist = nullptr;
+  int *d_ids_raw, *d_ids, *d_pos, *d_meta;
+  T* xkv;  // [Me_max][Ld*2d]
+  // Stage-I state
+  int *s_feed, *s_done, *s_nsteps, *s_forced, *s_anchors, *s_caps, *s_hist, *s_hist2, *s_rowseq, *s_parents;
+  double* s_score;
+  // outputs (device I/O staging)
+  int *o_tokens, *o_lens, *o_calls;
+  double* o_scores;
+  unsigned char* o_forced;
+  int* h_meta = nullptr;  // pinned staging for per-call metadata (one H2D copy)
+  int meta_cap;
+  cudaEvent_t meta_ev = nullptr;
+
+  // ---- arena ----
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  struct EncBufs {
+    float* x;
+    T *y, *qkv, *ctx, *hid;
+  } eb;
+  struct S1Bufs {
+    float* x;
+    T *y, *qkv, *qc, *ctx, *hid, *kc, *vc;
+    VocabParts parts;
+    float* logits;
+  } s1;
+  struct S2Bufs {
+    float* x;
+    T *y, *qkv, *qc, *ctx, *hid, *ymask;
+    int *ids, *pos, *out_row;
+    VocabParts parts;
+    RowStat* mstat;
+    float* logits;
+  } s2;
+
+  // protocol-face state
+  int p_rows = 0, p_cap = 0, p_len = 0, p_last_pos = -1, p_nseq = 0;
+  bool p_has_cache = false;
+  std::vector<int> p_seq_off, p_seq_len;  // encoded sequences (host copy)
+  int p_B = 0, p_T = 0;
+  float* p_logits = nullptr;  // [p_B*p_T][V] last parallel logits
+  size_t p_logits_cap = 0;
+  float* p_mem = nullptr;
+  size_t p_mem_cap = 0;
+
+  std::map<std::tuple<const void*, int, int, int, int>, CUtensorMap> tmaps;
+
+  Engine(const hrt_config& c, const float* params, int dev) {
+    cfg = c;
+    device = dev;
+    d = c.d_model;
+    ff = c.d_ff;
+    H = c.n_heads;
+    dh = d / H;
+    Le = c.enc_layers;
+    Ld = c.dec_layers;
+    V = c.vocab_size;
+    Lmax = c.max_len;
+    P = c.max_len + c.max_chunk + 1;
+    emb_scale = (float)std::sqrt((double)d);
+    att_scale = (float)(1.0 / std::sqrt((double)dh));
+    if (d <= 0 || ff <= 0 || H <= 0 || d % H || Le < 0 || Ld < 1 || V < 8 || Lmax < 1 || c.max_chunk < 1)
+      throw HrtError(HRT_ERR_INVALID, "invalid model shape");
+    if (d > 1024) throw HrtError(HRT_ERR_INVALID, "d_model > 1024 unsupported");
+    if (BF16 && (d % 64 || ff % 64))
+      throw HrtError(HRT_ERR_INVALID, "bf16 engine needs d_model and d_ff multiples of 64 (tcgen05 K tiles)");
+    CUDA_OK(cudaSetDevice(dev));
+    CUDA_OK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    load_weights(params);
+    size_capacity();
+    alloc_buffers();
+    CUDA_OK(cudaStreamSynchronize(stream));
+  }
+
+  ~Engine() override {
+    cudaSetDevice(device);
+    cudaFree(wblob);
+    cudaFree(vblob);
+    cudaFree(persist);
+    cudaFree(arena);
+    cudaFree(p_logits);
+    cudaFree(p_mem);
+    if (h_meta) cudaFreeHost(h_meta);
+    if (meta_ev) cudaEventDestroy(meta_ev);
+  }
+
+  // -------------------------------------------------------------------------
+  // weights: fp32 blob in model.py:146-181 order -> transposed K-major T
+  // matrices (QKV fused, all decoder cross-K/V fused) + fp32 vectors.
+  // -------------------------------------------------------------------------
+  void load_weights(const float* params) {
+    const int64_t n = param_count(cfg);
+    float* dsrc = nullptr;
+    CUDA_OK(cudaMalloc(&dsrc, n * sizeof(float)));
+    CUDA_OK(cudaMemcpy(dsrc, params, n * sizeof(float), cudaMemcpyHostToDevice));
+    // matrix storage
+    size_t mats = (size_t)V * d + (size_t)Le * (4 * d * d + 2 * d * ff) +
+                  (size_t)Ld * (8 * d * d + 2 * d * ff);
+    size_t vecs = (size_t)P * d + (size_t)Le * (4 * d + d + ff + d + 4 * d) + 2 * d +
+                  (size_t)Ld * (3 * d + d + d + d + ff + d + 6 * d + 2 * d) + 2 * d + 64;
+    CUDA_OK(cudaMalloc(&wblob, mats * sizeof(T) + 256));
+    CUDA_OK(cudaMalloc(&vblob, vecs * sizeof(float) + 4096));
+    stats.weight_bytes = (int64_t)(mats * sizeof(T) + vecs * sizeof(float));
+    T* wp = reinterpret_cast<T*>(wblob);
+    float* vp = reinterpret_cast<float*>(vblob);
+    auto tmat = [&](size_t cnt) {
+      T* r = wp;
+      wp += cnt;
+      return r;
+    };
+    auto tvec = [&](size_t cnt) {
+      float* r = vp;
+      vp += align_up(cnt, 16);
+      return r;
+    };
+    int64_t off = 0;
+    auto src = [&](int64_t cnt) {
+      const float* r = dsrc + off;
+      off += cnt;
+      return r;
+    };
+    // transpose (K x N row-major fp32) -> (N x K) T rows of dst
+    auto put_t = [&](const float* s, int K, int N, T* dst) {
+      transpose_convert(s, K, N, dst);
+    };
+    auto put_v = [&](const float* s, int cnt, float* dst) {
+      CUDA_OK(cudaMemcpyAsync(dst, s, cnt * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    };
+    E = tmat((size_t)V * d);
+    convert(src((int64_t)V * d), (size_t)V * d, E);
+    enc.resize(Le);
+    for (int i = 0; i < Le; ++i) {
+      EncW& w = enc[i];
+      w.wqkv = tmat((size_t)3 * d * d);
+      w.wo = tmat((size_t)d * d);
+      w.w1 = tmat((size_t)ff * d);
+      w.w2 = tmat((size_t)d * ff);
+      w.bqkv = tvec(3 * d);
+      w.bo = tvec(d);
+      w.b1 = tvec(ff);
+      w.b2 = tvec(d);
+      w.ln1g = tvec(d);
+      w.ln1b = tvec(d);
+      w.ln2g = tvec(d);
+      w.ln2b = tvec(d);
+      put_v(src(d), d, w.ln1g);
+      put_v(src(d), d, w.ln1b);
+      put_t(src((int64_t)d * d), d, d, w.wqkv);
+      put_t(src((int64_t)d * d), d, d, w.wqkv + (size_t)d * d);
+      put_t(src((int64_t)d * d), d, d, w.wqkv + (size_t)2 * d * d);
+      put_t(src((int64_t)d * d), d, d, w.wo);
+      put_v(src(d), d, w.bqkv);
+      put_v(src(d), d, w.bqkv + d);
+      put_v(src(d), d, w.bqkv + 2 * d);
+      put_v(src(d), d, w.bo);
+      put_v(src(d), d, w.ln2g);
+      put_v(src(d), d, w.ln2b);
+      put_t(src((int64_t)d * ff), d, ff, w.w1);
+      put_v(src(ff), ff, w.b1);
+      put_t(src((int64_t)ff * d), ff, d, w.w2);
+      put_v(src(d), d, w.b2);
+    }
+    enc_lng = tvec(d);
+    enc_lnb = tvec(d);
+    put_v(src(d), d, enc_lng);
+    put_v(src(d), d, enc_lnb);
+    dec.resize(Ld);
+    wxkv = tmat((size_t)Ld * 2 * d * d);
+    bxkv = tvec((size_t)Ld * 2 * d);
+    for (int i = 0; i < Ld; ++i) {
+      DecW& w = dec[i];
+      w.wqkv = tmat((size_t)3 * d * d);
+      w.wo = tmat((size_t)d * d);
+      w.wqc = tmat((size_t)d * d);
+      w.woc = tmat((size_t)d * d);
+      w.w1 = tmat((size_t)ff * d);
+      w.w2 = tmat((size_t)d * ff);
+      w.bqkv = tvec(3 * d);
+      w.bo = tvec(d);
+      w.bqc = tvec(d);
+      w.boc = tvec(d);
+      w.b1 = tvec(ff);
+      w.b2 = tvec(d);
+      w.ln1g = tvec(d);
+      w.ln1b = tvec(d);
+      w.ln2g = tvec(d);
+      w.ln2b = tvec(d);
+      w.ln3g = tvec(d);
+      w.ln3b = tvec(d);
+      put_v(src(d), d, w.ln1g);
+      put_v(src(d), d, w.ln1b);
+      put_t(src((int64_t)d * d), d, d, w.wqkv);
+      put_t(src((int64_t)d * d), d, d, w.wqkv + (size_t)d * d);
+      put_t(src((int64_t)d * d), d, d, w.wqkv + (size_t)2 * d * d);
+      put_t(src((int64_t)d * d), d, d, w.wo);
+      put_v(src(d), d, w.bqkv);
+      put_v(src(d), d, w.bqkv + d);
+      put_v(src(d), d, w.bqkv + 2 * d);
+      put_v(src(d), d, w.bo);
+      put_v(src(d), d, w.ln2g);
+      put_v(src(d), d, w.ln2b);
+      // cross attention: Q here, K/V into the fused all-layer cross-KV matrix
+      put_t(src((int64_t)d * d), d, d, w.wqc);
+      put_t(src((int64_t)d * d), d, d, wxkv + (size_t)(2 * i) * d * d);
+      put_t(src((int64_t)d * d), d, d, wxkv + (size_t)(2 * i + 1) * d * d);
+      put_t(src((int64_t)d * d), d, d, w.woc);
+      put_v(src(d), d, w.bqc);
+      put_v(src(d), d, bxkv + (size_t)2 * i * d);
+      put_v(src(d), d, bxkv + (size_t)(2 * i + 1) * d);
+      put_v(src(d), d, w.boc);
+      put_v(src(d), d, w.ln3g);
+      put_v(src(d), d, w.ln3b);
+      put_t(src((int64_t)d * ff), d, ff, w.w1);
+      put_v(src(ff), ff, w.b1);
+      put_t(src((int64_t)ff * d), ff, d, w.w2);
+      put_v(src(d), d, w.b2);
+    }
+    dec_lng = tvec(d);
+    dec_lnb = tvec(d);
+    put_v(src(d), d, dec_lng);
+    put_v(src(d), d, dec_lnb);
+    if (off != n) throw HrtError(HRT_ERR_INVALID, "parameter blob layout mismatch");
+    // positional table (model.py:104-112): angles in fp64, cast to fp32
+    std::vector<float> h_pe((size_t)P * d, 0.f);
+    for (int p = 0; p < P; ++p)
+      for (int i = 0; i < d / 2; ++i) {
+        double ang = (double)p / std::pow(10000.0, 2.0 * i / d);
+        h_pe[(size_t)p * d + 2 * i] = (float)std::sin(ang);
+        h_pe[(size_t)p * d + 2 * i + 1] = (float)std::cos(ang);
+      }
+    pe = tvec((size_t)P * d);
+    CUDA_OK(cudaMemcpyAsync(pe, h_pe.data(), h_pe.size() * sizeof(float), cudaMemcpyHostToDevice, stream));
+    CUDA_OK(cudaStreamSynchronize(stream));
+    cudaFree(dsrc);
+  }
+
+  static int64_t param_count(const hrt_config& c) {
+    int64_t d = c.d_model, f = c.d_ff;
+    int64_t attn = 4 * d * d + 4 * d, ln = 2 * d, ffn = 2 * d * f + f + d;
+    return (int64_t)c.vocab_size * d + c.enc_layers * (2 * ln + attn + ffn) + ln +
+           c.dec_layers * (3 * ln + 2 * attn + ffn) + ln;
+  }
+
+  void transpose_convert(const float* s, int K, int N, T* dst);
+  void convert(const float* s, size_t n, T* dst);
+
+  // -------------------------------------------------------------------------
+  // capacity + arena plan
+  // -------------------------------------------------------------------------
+  void size_capacity() {
+    Bmax = std::max(1, cfg.max_sentences);
+    beam_max = std::max(1, cfg.max_beam);
+    Me_max = cfg.max_src_tokens > 0 ? cfg.max_src_tokens : Bmax * Lmax;
+    R_max = Bmax * beam_max;
+    cap_max = Lmax + 1;  // AT mode (k = 1) worst case; skip-AT needs ceil(L/k)+1
+    M2_max = Bmax * beam_max * (Lmax + cfg.max_chunk);
+    Mm_max = M2_max;
+    nt_max = cdiv(V, 64);
+    logit_rows = 4096;
+  }
+
+  template <class Fn>
+  size_t plan_phases(char* base, Fn&& assign) {
+    size_t mx = 0;
+    for (int phase = 0; phase < 3; ++phase) {
+      Plan p;
+      assign(phase, p, base);
+      mx = std::max(mx, p.off);
+    }
+    return mx;
+  }
+
+  int nt_for_rows(int rows) const { return BF16 ? cdiv(V, choose_bn(rows, V)) : cdiv(V, 256); }
+
+  void carve(int phase, Plan& p, char* base) {
+    if (phase == 0) {
+      eb.x = p.take<float>(base, (size_t)Me_max * d);
+      eb.y = p.take<T>(base, (size_t)Me_max * d);
+      eb.qkv = p.take<T>(base, (size_t)Me_max * 3 * d);
+      eb.ctx = p.take<T>(base, (size_t)Me_max * d);
+      eb.hid = p.take<T>(base, (size_t)Me_max * ff);
+    } else if (phase == 1) {
+      s1.x = p.take<float>(base, (size_t)R_max * d);
+      s1.y = p.take<T>(base, (size_t)R_max * d);
+      s1.qkv = p.take<T>(base, (size_t)R_max * 3 * d);
+      s1.qc = p.take<T>(base, (size_t)R_max * d);
+      s1.ctx = p.take<T>(base, (size_t)R_max * d);
+      s1.hid = p.take<T>(base, (size_t)R_max * ff);
+      s1.kc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
+      s1.vc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
+      const size_t ntot = (size_t)std::max(R_max * nt_for_rows(R_max), std::min(R_max, 128) * nt_max);
+      s1.parts.mx = p.take<float>(base, ntot);
+      s1.parts.sum = p.take<float>(base, ntot);
+      s1.parts.val = p.take<float>(base, ntot * KTOP_MAX);
+      s1.parts.id = p.take<int>(base, ntot * KTOP_MAX);
+      s1.parts.eos = p.take<float>(base, R_max);
+      s1.logits = p.take<float>(base, (size_t)std::min(R_max, logit_rows) * V);
+    } else {
+      s2.x = p.take<float>(base, (size_t)M2_max * d);
+      s2.y = p.take<T>(base, (size_t)M2_max * d);
+      s2.qkv = p.take<T>(base, (size_t)M2_max * 3 * d);
+      s2.qc = p.take<T>(base, (size_t)M2_max * d);
+      s2.ctx = p.take<T>(base, (size_t)M2_max * d);
+      s2.hid = p.take<T>(base, (size_t)M2_max * ff);
+      s2.ymask = p.take<T>(base, (size_t)Mm_max * d);
+      s2.ids = p.take<int>(base, M2_max);
+      s2.pos = p.take<int>(base, M2_max);
+      s2.out_row = p.take<int>(base, M2_max);
+      const size_t ntot = (size_t)std::max(Mm_max * nt_for_rows(Mm_max), std::min(Mm_max, 128) * nt_max);
+      s2.parts.mx = p.take<float>(base, ntot);
+      s2.parts.sum = p.take<float>(base, ntot);
+      s2.parts.val = p.take<float>(base, ntot);  // KT = 1 in Stage II
+      s2.parts.id = p.take<int>(base, ntot);
+      s2.parts.eos = p.take<float>(base, Mm_max);
+      s2.mstat = p.take<RowStat>(base, Mm_max);
+      s2.logits = p.take<float>(base, (size_t)std::min(Mm_max, logit_rows) * V);
+    }
+  }
+
+  void alloc_buffers() {
+    // persistent region
+    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256;
+    auto persist_plan = [&](char* base) {
+      Plan p;
+      d_ids_raw = p.take<int>(base, Me_max + Bmax);
+      d_ids = p.take<int>(base, Me_max);
+      d_pos = p.take<int>(base, Me_max);
+      d_meta = p.take<int>(base, meta_cap);
+      xkv = p.take<T>(base, (size_t)Me_max * Ld * 2 * d);
+      s_feed = p.take<int>(base, R_max);
+      s_done = p.take<int>(base, R_max);
+      s_nsteps = p.take<int>(base, R_max);
+      s_forced = p.take<int>(base, R_max);
+      s_caps = p.take<int>(base, R_max);
+      s_rowseq = p.take<int>(base, R_max);
+      s_parents = p.take<int>(base, R_max);
+      s_anchors = p.take<int>(base, (size_t)R_max * cap_max);
+      s_hist = p.take<int>(base, (size_t)R_max * cap_max);
+      s_hist2 = p.take<int>(base, (size_t)R_max * cap_max);
+      s_score = p.take<double>(base, R_max);
+      o_tokens = p.take<int>(base, (size_t)Bmax * Lmax);
+      o_lens = p.take<int>(base, Bmax);
+      o_calls = p.take<int>(base, Bmax);
+      o_scores = p.take<double>(base, (size_t)Bmax * 3);
+      o_forced = p.take<unsigned char>(base, Bmax);
+      return p.off;
+    };
+    size_t pbytes = persist_plan(nullptr);
+    CUDA_OK(cudaMalloc(&persist, pbytes));
+    persist_plan(persist);
+    arena_bytes = 0;
+    for (int ph = 0; ph < 3; ++ph) {
+      Plan p;
+      carve(ph, p, nullptr);
+      arena_bytes = std::max(arena_bytes, p.off);
+    }
+    cudaError_t e = cudaMalloc(&arena, arena_bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw HrtError(HRT_ERR_MEMORY, "device arena of " + std::to_string(arena_bytes) + " bytes: " +
+                                         cudaGetErrorString(e));
+    }
+    for (int ph = 0; ph < 3; ++ph) {
+      Plan p;
+      carve(ph, p, arena);
+    }
+    stats.arena_bytes = (int64_t)(arena_bytes + pbytes);
+    CUDA_OK(cudaMallocHost(&h_meta, (size_t)meta_cap * sizeof(int)));
+    CUDA_OK(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming));
+    CUDA_OK(cudaEventRecord(meta_ev, stream));
+  }
+
+  // -------------------------------------------------------------------------
+  // kernel launch wrappers
+  // -------------------------------------------------------------------------
+  const CUtensorMap& tmap(const void* p, int rows, int cols, int ld, int box) {
+    auto key = std::make_tuple(p, rows, cols, ld, box);
+    auto it = tmaps.find(key);
+    if (it != tmaps.end()) return it->second;
+    return tmaps.emplace(key, make_tmap_bf16_kmajor(p, rows, cols, ld, box)).first->second;
+  }
+
+  template <int BN, int ST, class Epi>
+  void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+    if constexpr (BF16) {
+      auto kern = tc_gemm_kernel<BN, ST, Epi>;
+      static bool attr = false;
+      const int smem = TcSmem<BN, ST>::TOTAL;
+      if (!attr) {
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+      }
+      const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
+      const CUtensorMap& tb = tmap(W, N, K, K, BN);
+      dim3 grid(cdiv(N, BN), cdiv(M, TC_BM));
+      kern<<<grid, TC_THREADS, smem, stream>>>(ta, tb, M, N, K, M_dev, epi);
+    }
+  }
+
+  int choose_bn(int M, int N) const {
+    if (M <= 128) return 64;
+    if (N >= 4096) return 256;
+    return 128;
+  }
+
+  // C[M,N] = A[M,K] . W[N,K]^T with a fused epilogue
+  template <class Epi>
+  void gemm(int cls, const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi,
+            const int* M_dev = nullptr, int bn = 0) {
+    if (M <= 0) return;
+    Scope sc(this, cls, (double)sizeof(T) * ((double)N * K + (double)M * K), 2.0 * M * N * K);
+    if constexpr (BF16) {
+      if (bn == 0) bn = choose_bn(M, N);
+      if (bn == 64)
+        tc_launch<64, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+      else if (bn == 128)
+        tc_launch<128, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+      else
+        tc_launch<256, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+    } else {
+      dim3 grid(cdiv(N, SG_BN), cdiv(M, SG_BM));
+      simt_gemm_kernel<T, Epi><<<grid, SG_THREADS, 0, stream>>>(A, lda, W, K, M, N, K, M_dev, epi);
+    }
+    check_launch();
+  }
+
+  template <int NPL>
+  void ln_launch(const float* x, int M, const float* g, const float* b, T* y, const int* out_row, float* y32) {
+    layernorm_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(x, nullptr, M, d, g, b, y, out_row, y32);
+  }
+  void layernorm(const float* x, int M, const float* g, const float* b, T* y, const int* out_row = nullptr,
+                 float* y32 = nullptr) {
+    if (M <= 0) return;
+    Scope sc(this, K_OTHER, (double)M * d * (4 + sizeof(T)), 8.0 * M * d);
+    const int npl = cdiv(d, 32);
+    if (npl <= 1) ln_launch<1>(x, M, g, b, y, out_row, y32);
+    else if (npl <= 2) ln_launch<2>(x, M, g, b, y, out_row, y32);
+    else if (npl <= 4) ln_launch<4>(x, M, g, b, y, out_row, y32);
+    else if (npl <= 8) ln_launch<8>(x, M, g, b, y, out_row, y32);
+    else if (npl <= 16) ln_launch<16>(x, M, g, b, y, out_row, y32);
+    else ln_launch<32>(x, M, g, b, y, out_row, y32);
+    check_launch();
+  }
+
+  template <int NPL>
+  void emb_launch(const int* ids, const int* pos, int pc, int M, const float* g, const float* b, float* x, T* y) {
+    embed_ln_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(ids, pos, pc, nullptr, M, d, emb_scale, E, pe, g, b, x, y);
+  }
+  void embed_ln(const int* ids, const int* pos, int pos_const, int M, const float* g, const float* b, float* x, T* y) {
+    if (M <= 0) return;
+    Scope sc(this, K_OTHER, (double)M * d * (4 + 4 + 2 * sizeof(T)), 8.0 * M * d);
+    const int npl = cdiv(d, 32);
+    if (npl <= 1) emb_launch<1>(ids, pos, pos_const, M, g, b, x, y);
+    else if (npl <= 2) emb_launch<2>(ids, pos, pos_const, M, g, b, x, y);
+    else if (npl <= 4) emb_launch<4>(ids, pos, pos_const, M, g, b, x, y);
+    else if (npl <= 8) emb_launch<8>(ids, pos, pos_const, M, g, b, x, y);
+    else if (npl <= 16) emb_launch<16>(ids, pos, pos_const, M, g, b, x, y);
+    else emb_launch<32>(ids, pos, pos_const, M, g, b, x, y);
+    check_launch();
+  }
+
+  // ragged whole-sequence attention (see attn_prefill_kernel)
+  void attn_prefill(const T* q, int qs, const T* k, const T* v, int kvs, T* out, int os, int nseq, int max_slot,
+                    int lk_max, const int* q_off, const int* q_slot, const int* q_len, const int* kv_map,
+                    const int* kv_off, const int* kv_len, const unsigned char* key_ok, int causal, double flops) {
+    if (nseq <= 0 || max_slot <= 0) return;
+    lk_max = std::max(lk_max, 1);
+    Scope sc(this, K_ATTN, 0.0, flops);
+    const int nwarp = 8;
+    const size_t smem = (size_t)(2 * dh * lk_max + lk_max + nwarp * lk_max + nwarp * dh) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    if (smem > 227 * 1024) throw HrtError(HRT_ERR_INVALID, "attention key length too large for shared memory");
+    dim3 grid(nseq, H, cdiv(max_slot, nwarp * 8));
+    attn_prefill_kernel<T><<<grid, nwarp * 32, smem, stream>>>(q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map,
+                                                               kv_off, kv_len, key_ok, causal, dh, lk_max,
+                                                               att_scale);
+    check_launch();
+  }
+
+  template <bool SELF>
+  void attn_decode(const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc, const int* hist, int cap, int t,
+                   const int* row_seq, const int* kv_off, const int* kv_len, int R, int lk_max, T* out,
+                   double bytes) {
+    if (R <= 0) return;
+    Scope sc(this, K_ATTN, bytes, 0.0);
+    const int nwarp = 4;
+    const size_t smem = (size_t)nwarp * (lk_max + dh) * sizeof(float);
+    attn_decode_kernel<T, SELF><<<cdiv(R * H, nwarp), nwarp * 32, smem, stream>>>(
+        q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, row_seq, kv_off, kv_len, nullptr, R, H, dh, lk_max, att_scale,
+        out, d);
+    check_launch();
+  }
+
+  // vocab projection of R rows of y (K-major d) into tile partials.
+  void vocab_parts(const T* y, int y_cap, int R, VocabParts& parts, int kt, int norm_allowed, float* logits_buf) {
+    if (R <= 0) return;
+    if constexpr (BF16) {
+      const int bn = choose_bn(R, V);
+      parts.ntiles = cdiv(V, bn);
+      Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
+      if (kt == 1) {
+        VocabEpi<1> epi{parts, norm_allowed, bn};
+        launch_vocab(y, y_cap, R, epi, bn);
+      } else {
+        VocabEpi<KTOP_MAX> epi{parts, norm_allowed, bn};
+        launch_vocab(y, y_cap, R, epi, bn);
+      }
+      check_launch();
+    } else {
+      // fp32: materialise logits in row blocks, then reduce per 256-col tile
+      parts.ntiles = cdiv(V, 256);
+      for (int r0 = 0; r0 < R; r0 += logit_rows) {
+        const int rn = std::min(logit_rows, R - r0);
+        {
+          Scope sc(this, K_VOCAB | K_GEMM, 4.0 * ((double)V * d + (double)rn * d + (double)rn * V),
+                   2.0 * rn * (double)V * d);
+          EpiStoreF32 epi{logits_buf, V};
+          dim3 grid(cdiv(V, SG_BN), cdiv(rn, SG_BM));
+          simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y + (size_t)r0 * d, d, E, d, rn, V, d,
+                                                                            nullptr, epi);
+          check_launch();
+        }
+        VocabParts sub = parts;
+        sub.mx += (size_t)r0 * parts.ntiles;
+        sub.sum += (size_t)r0 * parts.ntiles;
+        sub.val += (size_t)r0 * parts.ntiles * kt;
+        sub.id += (size_t)r0 * parts.ntiles * kt;
+        sub.eos += r0;
+        Scope sc(this, K_OTHER, 4.0 * rn * V, 0);
+        dim3 grid(rn, parts.ntiles);
+        if (kt == 1)
+          rowstats_from_logits_kernel<1><<<grid, 32, 0, stream>>>(logits_buf, V, V, nullptr, sub, 256, norm_allowed);
+        else
+          rowstats_from_logits_kernel<KTOP_MAX>
+              <<<grid, 32, 0, stream>>>(logits_buf, V, V, nullptr, sub, 256, norm_allowed);
+        check_launch();
+      }
+    }
+  }
+  template <class Epi>
+  void launch_vocab(const T* y, int y_cap, int R, const Epi& epi, int bn) {
+    if (bn == 64)
+      tc_launch<64, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+    else if (bn == 128)
+      tc_launch<128, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+    else
+      tc_launch<256, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+  }
+
+  // full fp32 logits of R rows (protocol face / parity), chunked
+  void full_logits(const T* y, int y_cap, int R, float* dst) {
+    Scope sc(this, K_VOCAB | K_GEMM, sizeof(T) * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
+    EpiStoreF32 epi{dst, V};
+    if constexpr (BF16) {
+      launch_vocab(y, y_cap, R, epi, choose_bn(R, V));
+    } else {
+      dim3 grid(cdiv(V, SG_BN), cdiv(R, SG_BM));
+      simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y, d, E, d, R, V, d, nullptr, epi);
+    }
+    check_launch();
+  }
+
+  // -------------------------------------------------------------------------
+  // phase 1: encoder over packed sources (infer.py:176-221), then the fused
+  // cross-K/V projection of every decoder layer (infer.py:216-220).
+  // d_ids / d_pos hold the packed tokens; seq metadata in device arrays.
+  // -------------------------------------------------------------------------
+  void run_encoder(int M, int nseq, int max_len_seq, const int* off, const int* len) {
+    if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed max_src_tokens");
+    if (Le > 0)
+      embed_ln(d_ids, d_pos, 0, M, enc[0].ln1g, enc[0].ln1b, eb.x, eb.y);
+    else
+      embed_ln(d_ids, d_pos, 0, M, enc_lng, enc_lnb, eb.x, eb.y);
+    for (int i = 0; i < Le; ++i) {
+      const EncW& w = enc[i];
+      gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
+      attn_prefill(eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, nseq, max_len_seq, max_len_seq, off,
+                   len, len, nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
+      gemm(K_GEMM, eb.ctx, Me_max, d, M, w.wo, d, d, EpiResidual{eb.x, d, w.bo});
+      layernorm(eb.x, M, w.ln2g, w.ln2b, eb.y);
+      gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
+      gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
+      if (i + 1 < Le)
+        layernorm(eb.x, M, enc[i + 1].ln1g, enc[i + 1].ln1b, eb.y);
+      else
+        layernorm(eb.x, M, enc_lng, enc_lnb, eb.y, nullptr, p_mem_target);
+    }
+    gemm(K_GEMM, eb.y, Me_max, d, M, wxkv, Ld * 2 * d, d, EpiBiasT<T, false>{xkv, Ld * 2 * d, bxkv});
+  }
+  float* p_mem_target = nullptr;
+
+  // -------------------------------------------------------------------------
+  // one Stage-I decoder call for rows 0..R-1 at position `pos`, cache slot t
+  // (infer.py:234-301 up to the final LN; vocab handled by the caller)
+  // -------------------------------------------------------------------------
+  void decoder_step(int R, int t, int pos, int cap, const int* feed, const int* hist, const int* row_seq,
+                    const int* kv_off, const int* kv_len, int max_src) {
+    embed_ln(feed, nullptr, pos, R, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
+    for (int i = 0; i < Ld; ++i) {
+      const DecW& w = dec[i];
+      T* kc = s1.kc + (size_t)i * R_max * cap_max * d;
+      T* vc = s1.vc + (size_t)i * R_max * cap_max * d;
+      gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv});
+      attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
+                        nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d);
+      gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo});
+      layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y);
+      gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc});
+      attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
+                         nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
+                         2.0 * sizeof(T) * (double)R * max_src * d);
+      gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc});
+      layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y);
+      gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1});
+      gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2});
+      if (i + 1 < Ld)
+        layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y);
+      else
+        layernorm(s1.x, R, dec_lng, dec_lnb, s1.y);
+    }
+  }
+
+  // -------------------------------------------------------------------------
+  // one parallel (Stage-II) decoder pass over packed candidate slots
+  // (infer.py:322-396). Leaves the final-LN'd rows in s2.y (or, with
+  // out_row, gathered into s2.ymask).
+  // -------------------------------------------------------------------------
+  void decoder_parallel(int M2, int nc, int max_slot, int max_src, const int* off, const int* slot,
+                        const int* qlen, const int* kv_map, const int* src_off, const int* src_len,
+                        const unsigned char* key_ok, int causal, const int* out_row) {
+    embed_ln(s2.ids, s2.pos, 0, M2, dec[0].ln1g, dec[0].ln1b, s2.x, s2.y);
+    for (int i = 0; i < Ld; ++i) {
+      const DecW& w = dec[i];
+      gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s2.qkv, 3 * d, w.bqkv});
+      attn_prefill(s2.qkv, 3 * d, s2.qkv + d, s2.qkv + 2 * d, 3 * d, s2.ctx, d, nc, max_slot, max_slot, off, slot,
+                   qlen, nullptr, off, qlen, key_ok, causal, 4.0 * d * (double)max_slot * M2);
+      gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.wo, d, d, EpiResidual{s2.x, d, w.bo});
+      layernorm(s2.x, M2, w.ln2g, w.ln2b, s2.y);
+      gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqc, d, d, EpiBiasT<T, false>{s2.qc, d, w.bqc});
+      attn_prefill(s2.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, s2.ctx, d, nc,
+                   max_slot, max_src, off, slot, qlen, kv_map, src_off, src_len, nullptr, 0,
+                   4.0 * d * (double)max_src * M2);
+      gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.woc, d, d, EpiResidual{s2.x, d, w.boc});
+      layernorm(s2.x, M2, w.ln3g, w.ln3b, s2.y);
+      gemm(K_GEMM, s2.y, M2_max, d, M2, w.w1, ff, d, EpiBiasT<T, true>{s2.hid, ff, w.b1});
+      gemm(K_GEMM, s2.hid, M2_max, ff, M2, w.w2, d, ff, EpiResidual{s2.x, d, w.b2});
+      if (i + 1 < Ld)
+        layernorm(s2.x, M2, dec[i + 1].ln1g, dec[i + 1].ln1b, s2.y);
+      else if (out_row)
+        layernorm(s2.x, M2, dec_lng, dec_lnb, s2.ymask, out_row);
+      else
+        layernorm(s2.x, M2, dec_lng, dec_lnb, s2.y);
+    }
+  }
+
+  // metadata upload: host vector -> d_meta (one H2D copy), returns device ptrs
+  int* meta_put(size_t& cursor, const std::vector<int>& v) {
+    const size_t o = cursor;
+    if (o + v.size() > (size_t)meta_cap) throw HrtError(HRT_ERR_MEMORY, "metadata buffer overflow");
+    std::copy(v.begin(), v.end(), h_meta + o);
+    cursor += v.size();
+    cursor = (cursor + 7) & ~size_t(7);
+    return d_meta + o;
+  }
+  void meta_flush(size_t cursor) {
+    CUDA_OK(cudaMemcpyAsync(d_meta, h_meta, cursor * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CUDA_OK(cudaEventRecord(meta_ev, stream));
+  }
+  // the previous call's metadata copy must have left the pinned buffer
+  void meta_reset() { CUDA_OK(cudaEventSynchronize(meta_ev)); }
+
+  // -------------------------------------------------------------------------
+  // session protocol
+  // -------------------------------------------------------------------------
+  void encode(const int32_t* ids, const int32_t* lens, int n, float* mem_out) override {
+    if (n < 1 || n > Bmax) throw HrtError(HRT_ERR_INVALID, "n_seq out of range");
+    std::vector<int> off(n + 1, 0), len(n);
+    int maxl = 0;
+    for (int i = 0; i < n; ++i) {
+      if (lens[i] < 1) throw HrtError(HRT_ERR_INFERENCE, "empty source");
+      if (lens[i] > Lmax)
+        throw HrtError(HRT_ERR_INFERENCE, "source length " + std::to_string(lens[i]) + " exceeds max_len " +
+                                              std::to_string(Lmax));
+      len[i] = lens[i];
+      off[i + 1] = off[i] + lens[i];
+      maxl = std::max(maxl, lens[i]);
+    }
+    const int M = off[n];
+    if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed capacity");
+    std::vector<int> pos(M);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < len[i]; ++j) pos[off[i] + j] = j;
+    meta_reset();
+    size_t cur = 0;
+    int* d_off = meta_put(cur, off);
+    int* d_len = meta_put(cur, len);
+    meta_flush(cur);
+    CUDA_OK(cudaMemcpyAsync(d_ids, ids, M * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CUDA_OK(cudaMemcpyAsync(d_pos, pos.data(), M * sizeof(int), cudaMemcpyHostToDevice, stream));
+    // keep encoded-sequence metadata on device for later protocol calls
+    p_seq_off = off;
+    p_seq_len = len;
+    p_nseq = n;
+    if (mem_out) {
+      if (p_mem_cap < (size_t)M * d) {
+        cudaFree(p_mem);
+        CUDA_OK(cudaMalloc(&p_mem, (size_t)M * d * sizeof(float)));
+        p_mem_cap = (size_t)M * d;
+      }
+      p_mem_target = p_mem;
+    }
+    run_encoder(M, n, maxl, d_off, d_len);
+    p_mem_target = nullptr;
+    if (Le == 0 && mem_out) throw HrtError(HRT_ERR_INVALID, "memory output needs enc_layers >= 1");
+    if (mem_out) {
+      CUDA_OK(cudaMemcpyAsync(mem_out, p_mem, (size_t)M * d * sizeof(float), cudaMemcpyDeviceToHost, stream));
+    }
+    CUDA_OK(cudaStreamSynchronize(stream));
+    p_has_cache = false;
+  }
+
+  // device copies of encoded-sequence metadata for protocol calls
+  int *p_doff = nullptr, *p_dlen = nullptr;
+  void upload_seq_meta(size_t& cur, std::vector<int>& extra_unused) {
+    (void)extra_unused;
+    p_doff = meta_put(cur, p_seq_off);
+    p_dlen = meta_put(cur, p_seq_len);
+  }
+
+  std::vector<int> p_rowseq_h;
+  void start_cache(int rows, int cap, const int32_t* row_seq) override {
+    if (p_nseq == 0) throw HrtError(HRT_ERR_INFERENCE, "encode() must precede start_cache()");
+    if (rows < 1 || rows > R_max) throw HrtError(HRT_ERR_INVALID, "rows out of range");
+    if (cap < 1 || cap > cap_max) throw HrtError(HRT_ERR_INVALID, "cache capacity out of range");
+    p_rows = rows;
+    p_cap = cap;
+    p_len = 0;
+    p_last_pos = -1;
+    p_has_cache = true;
+    p_rowseq_h.assign(rows, 0);
+    if (row_seq)
+      for (int r = 0; r < rows; ++r) {
+        if (row_seq[r] < 0 || row_seq[r] >= p_nseq) throw HrtError(HRT_ERR_INVALID, "row_seq out of range");
+        p_rowseq_h[r] = row_seq[r];
+      }
+    CUDA_OK(cudaMemcpyAsync(s_rowseq, p_rowseq_h.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream));
+    stage1_init_kernel<<<cdiv(rows, 128), 128, 0, stream>>>(rows, cap, BOS_ID, s_feed, s_done, s_nsteps, s_forced,
+                                                           s_score, s_hist);
+    check_launch();
+    stats.kernel_launches++;
+  }
+
+  void step(const int32_t* tokens, int position, float* logp_out) override {
+    if (!p_has_cache) throw HrtError(HRT_ERR_INFERENCE, "start_cache() must precede step()");
+    if (p_last_pos >= 0 && position <= p_last_pos)
+      throw HrtError(HRT_ERR_INFERENCE, "new position must exceed all cached positions");
+    if (p_len >= p_cap) throw HrtError(HRT_ERR_INFERENCE, "decoder cache capacity exceeded");
+    if (position < 0 || position >= P) throw HrtError(HRT_ERR_INFERENCE, "position exceeds the positional table");
+    for (int r = 0; r < p_rows; ++r)
+      if (tokens[r] < 0 || tokens[r] >= V) throw HrtError(HRT_ERR_INVALID, "token id out of range");
+    meta_reset();
+    size_t cur = 0;
+    std::vector<int> dummy;
+    upload_seq_meta(cur, dummy);
+    meta_flush(cur);
+    CUDA_OK(cudaMemcpyAsync(s_feed, tokens, p_rows * sizeof(int), cudaMemcpyHostToDevice, stream));
+    int max_src = *std::max_element(p_seq_len.begin(), p_seq_len.end());
+    decoder_step(p_rows, p_len, position, p_cap, s_feed, s_hist, s_rowseq, p_doff, p_dlen, max_src);
+    if (logp_out) {
+      for (int r0 = 0; r0 < p_rows; r0 += logit_rows) {
+        const int rn = std::min(logit_rows, p_rows - r0);
+        full_logits(s1.y + (size_t)r0 * d, R_max - r0, rn, s1.logits);
+        logsoftmax_rows_kernel<<<rn, 256, 0, stream>>>(s1.logits, V, V);
+        check_launch();
+        stats.kernel_launches++;
+        CUDA_OK(cudaMemcpyAsync(logp_out + (size_t)r0 * V, s1.logits, (size_t)rn * V * sizeof(float),
+                                cudaMemcpyDeviceToHost, stream));
+      }
+    }
+    CUDA_OK(cudaStreamSynchronize(stream));
+    p_len += 1;
+    p_last_pos = position;
+    stats.decoder_calls += 1;
+  }
+
+  void reorder(const int32_t* parents) override {
+    if (!p_has_cache) throw HrtError(HRT_ERR_INFERENCE, "start_cache() must precede reorder()");
+    bool ident = true;
+    for (int r = 0; r < p_rows; ++r) {
+      if (parents[r] < 0 || parents[r] >= p_rows) throw HrtError(HRT_ERR_INVALID, "parent row out of range");
+      ident &= parents[r] == r;
+    }
+    if (ident) return;
+    CUDA_OK(cudaMemcpyAsync(s_parents, parents, p_rows * sizeof(int), cudaMemcpyHostToDevice, stream));
+    reorder_hist_kernel<<<p_rows, 128, 0, stream>>>(s_parents, s_hist, s_hist2, p_rows, p_cap, p_len);
+    check_launch();
+    stats.kernel_launches++;
+    std::swap(s_hist, s_hist2);
+    CUDA_OK(cudaStreamSynchronize(stream));
+  }
+
+  void parallel_logits(const int32_t* ids, const int32_t* pos, const uint8_t* pad, int B, int Tn, int mode,
+                       const int32_t* seq, float* logits_out) override {
+    if (p_nseq == 0) throw HrtError(HRT_ERR_INFERENCE, "encode() must precede parallel_logits()");
+    if (B < 1 || Tn < 1) throw HrtError(HRT_ERR_INVALID, "empty parallel batch");
+    if (mode != 0 && mode != 1) throw HrtError(HRT_ERR_INFERENCE, "unknown mode");
+    const int M2 = B * Tn;
+    if (M2 > M2_max) throw HrtError(HRT_ERR_MEMORY, "parallel batch exceeds capacity");
+    for (int i = 0; i < M2; ++i) {
+      if (pos[i] < 0 || pos[i] >= P) throw HrtError(HRT_ERR_INVALID, "position exceeds the positional table");
+      if (ids[i] < 0 || ids[i] >= V) throw HrtError(HRT_ERR_INVALID, "token id out of range");
+    }
+    std::vector<int> off(B + 1), slot(B, Tn), qlen(B, Tn), kvmap(B, 0);
+    for (int b = 0; b <= B; ++b) off[b] = b * Tn;
+    if (seq)
+      for (int b = 0; b < B; ++b) {
+        if (seq[b] < 0 || seq[b] >= p_nseq) throw HrtError(HRT_ERR_INVALID, "seq out of range");
+        kvmap[b] = seq[b];
+      }
+    meta_reset();
+    size_t cur = 0;
+    int* d_off = meta_put(cur, off);
+    int* d_slot = meta_put(cur, slot);
+    int* d_qlen = meta_put(cur, qlen);
+    int* d_map = meta_put(cur, kvmap);
+    std::vector<int> dummy;
+    upload_seq_meta(cur, dummy);
+    // key mask bytes packed into ints region
+    unsigned char* d_keyok = nullptr;
+    if (pad) {
+      std::vector<int> packed((M2 + 3) / 4, 0);
+      std::memcpy(packed.data(), pad, M2);
+      d_keyok = reinterpret_cast<unsigned char*>(meta_put(cur, packed));
+    }
+    meta_flush(cur);
+    CUDA_OK(cudaMemcpyAsync(s2.ids, ids, M2 * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CUDA_OK(cudaMemcpyAsync(s2.pos, pos, M2 * sizeof(int), cudaMemcpyHostToDevice, stream));
+    int max_src = *std::max_element(p_seq_len.begin(), p_seq_len.end());
+    decoder_parallel(M2, B, Tn, max_src, d_off, d_slot, d_qlen, d_map, p_doff, p_dlen, d_keyok, mode, nullptr);
+    if (p_logits_cap < (size_t)M2 * V) {
+      cudaFree(p_logits);
+      CUDA_OK(cudaMalloc(&p_logits, (size_t)M2 * V * sizeof(float)));
+      p_logits_cap = (size_t)M2 * V;
+    }
+    full_logits(s2.y, M2_max, M2, p_logits);
+    if (logits_out)
+      CUDA_OK(cudaMemcpyAsync(logits_out, p_logits, (size_t)M2 * V * sizeof(float), cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaStreamSynchronize(stream));
+    p_B = B;
+    p_T = Tn;
+    stats.decoder_calls += 1;
+  }
+
+  void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) override;
+
+  void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
+                 const int32_t* caps, const hrt_translate_out* out, int on_device) override;
+};
+
+// ---------------------------------------------------------------------------
+// weight conversion kernels
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void transpose_convert_kernel(const float* __restrict__ s, int K, int N, T* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? s[(size_t)k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) dst[(size_t)n * K + k] = from_f<T>(tile[threadIdx.x][i]);
+  }
+}
+
+template <typename T>
+__global__ void convert_kernel(const float* __restrict__ s, size_t n, T* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = from_f<T>(s[i]);
+}
+
+template <typename T>
+void Engine<T>::transpose_convert(const float* s, int K, int N, T* dst) {
+  dim3 grid(cdiv(N, 32), cdiv(K, 32));
+  transpose_convert_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(s, K, N, dst);
+  check_launch();
+}
+template <typename T>
+void Engine<T>::convert(const float* s, size_t n, T* dst) {
+  convert_kernel<T><<<1024, 256, 0, stream>>>(s, n, dst);
+  check_launch();
+}
+
+// argmax / renormalised log-prob over non-excluded ids (infer.py:401-418)
+__global__ void argmax_lp_kernel(const float* __restrict__ logits, int V, const unsigned char* __restrict__ excl,
+                                 int* __restrict__ amax, float* __restrict__ lp) {
+  const int row = blockIdx.x;
+  const float* l = logits + (size_t)row * V;
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    if (excl && excl[c]) continue;
+    if (better(l[c], c, bv, bi)) {
+      bv = l[c];
+      bi = c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (better(sv[w], si[w], bv, bi)) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    sv[0] = bv;
+    si[0] = bi;
+  }
+  __syncthreads();
+  const float m = sv[0];
+  float s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x)
+    if (!(excl && excl[c])) s += expf(l[c] - m);
+  s = warp_sum(s);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sv[w];
+    amax[row] = si[0];
+    lp[row] = -logf(t);
+  }
+}
+
+template <typename T>
+void Engine<T>::argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) {
+  if (p_B == 0) throw HrtError(HRT_ERR_INFERENCE, "parallel_logits() must precede argmax_logprobs()");
+  const int M2 = p_B * p_T;
+  meta_reset();
+  size_t cur = 0;
+  unsigned char* d_ex = nullptr;
+  if (excl && n_excl > 0) {
+    std::vector<unsigned char> m(V, 0);
+    for (int i = 0; i < n_excl; ++i) {
+      if (excl[i] < 0 || excl[i] >= V) throw HrtError(HRT_ERR_INVALID, "excluded id out of range");
+      m[excl[i]] = 1;
+    }
+    std::vector<int> packed((V + 3) / 4, 0);
+    std::memcpy(packed.data(), m.data(), V);
+    d_ex = reinterpret_cast<unsigned char*>(meta_put(cur, packed));
+  }
+  int* d_amax = meta_put(cur, std::vector<int>(M2, 0));
+  float* d_lp = reinterpret_cast<float*>(meta_put(cur, std::vector<int>(M2, 0)));
+  meta_flush(cur);
+  argmax_lp_kernel<<<M2, 256, 0, stream>>>(p_logits, V, d_ex, d_amax, d_lp);
+  check_launch();
+  stats.kernel_launches++;
+  CUDA_OK(cudaMemcpyAsync(amax, d_amax, M2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CUDA_OK(cudaMemcpyAsync(lp, d_lp, M2 * sizeof(float), cudaMemcpyDeviceToHost, stream));
+  CUDA_OK(cudaStreamSynchronize(stream));
+}
+
+// ---------------------------------------------------------------------------
+// fused production path: hrt_translate for a batch (decoding.py:249-302)
+// ---------------------------------------------------------------------------
+template <typename T>
+void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
+                          const int32_t* caps, const hrt_translate_out* out, int on_device) {
+  if (B < 1 || B > Bmax) throw HrtError(HRT_ERR_INVALID, "batch size out of range");
+  if (k < 2 || k > cfg.max_chunk) throw HrtError(HRT_ERR_DECODING, "chunk size k not supported by the engine");
+  if (b_nat < 1 || b_at < b_nat) throw HrtError(HRT_ERR_DECODING, "need b_at >= b_nat >= 1");
+  if (b_at > beam_max) throw HrtError(HRT_ERR_INVALID, "b_at exceeds engine max_beam");
+  if (b_at != 1) throw HrtError(HRT_ERR_INVALID, "fused path: beam search not yet available (use b_at=1)");
+  // ---- host schedule: truncate (decoding.py:260), caps, sort by cap desc ----
+  std::vector<int> raw_off(B + 1, 0), S(B), cap(B);
+  for (int i = 0; i < B; ++i) {
+    if (lens[i] < 1) throw HrtError(HRT_ERR_INVALID, "empty source");
+    raw_off[i + 1] = raw_off[i] + lens[i];
+    S[i] = std::min<int>(lens[i], Lmax);
+    cap[i] = caps ? caps[i] : cdiv(Lmax, k);
+    if (cap[i] < 1) throw HrtError(HRT_ERR_INVALID, "max_steps must be >= 1");
+    if (cap[i] + 1 > cap_max || k * cap[i] + 1 > P)
+      throw HrtError(HRT_ERR_INVALID, "max_steps exceeds the positional table / cache capacity");
+  }
+  if (raw_off[B] > Me_max + Bmax) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed capacity");
+  std::vector<int> perm(B);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cap[a] > cap[b]; });
+  std::vector<int> off(B + 1, 0), len(B), capS(B), slot(B), off2(B + 1, 0), moff(B + 1, 0);
+  int max_src = 0, max_cap = 0, max_slot = 0;
+  for (int i = 0; i < B; ++i) {
+    const int p = perm[i];
+    len[i] = S[p];
+    off[i + 1] = off[i] + S[p];
+    capS[i] = cap[p];
+    slot[i] = k * cap[p];
+    off2[i + 1] = off2[i] + slot[i];
+    moff[i + 1] = moff[i] + (slot[i] - slot[i] / k);
+    max_src = std::max(max_src, S[p]);
+    max_cap = std::max(max_cap, cap[p]);
+    max_slot = std::max(max_slot, slot[i]);
+  }
+  const int Mtok = off[B];
+  if (Mtok > Me_max) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed max_src_tokens");
+  const int M2 = off2[B], Mm = moff[B];
+  if (M2 > M2_max) throw HrtError(HRT_ERR_MEMORY, "stage-II rows exceed capacity");
+  // rows alive at step t: prefix of the cap-sorted batch
+  std::vector<int> alive(max_cap, 0);
+  for (int t = 0, r = B; t < max_cap; ++t) {
+    while (r > 0 && capS[r - 1] <= t) --r;
+    alive[t] = r;
+  }
+  // mask-row map for the final Stage-II LayerNorm gather
+  std::vector<int> out_row(M2, -1), seqmap(B), cand_beg(B + 1);
+  for (int i = 0; i < B; ++i) {
+    for (int j = 0; j < slot[i]; ++j)
+      if ((j + 1) % k != 0) out_row[off2[i] + j] = moff[i] + j - (j + 1) / k;
+    seqmap[i] = i;
+    cand_beg[i] = i;
+  }
+  cand_beg[B] = B;
+  meta_reset();
+  size_t cur = 0;
+  int* d_rawoff = meta_put(cur, raw_off);
+  int* d_perm = meta_put(cur, perm);
+  int* d_off = meta_put(cur, off);
+  int* d_len = meta_put(cur, len);
+  int* d_caps = meta_put(cur, capS);
+  int* d_slot = meta_put(cur, slot);
+  int* d_off2 = meta_put(cur, off2);
+  int* d_moff = meta_put(cur, moff);
+  int* d_seqmap = meta_put(cur, seqmap);
+  int* d_cbeg = meta_put(cur, cand_beg);
+  int* d_qlen2 = meta_put(cur, std::vector<int>(B, 0));
+  int* d_outrow = meta_put(cur, out_row);
+  meta_flush(cur);
+  const int* src_ids = ids;
+  if (!on_device) {
+    CUDA_OK(cudaMemcpyAsync(d_ids_raw, ids, raw_off[B] * sizeof(int), cudaMemcpyHostToDevice, stream));
+    src_ids = d_ids_raw;
+  }
+  {
+    Scope sc(this, K_OTHER, 8.0 * Mtok, 0);
+    gather_sentences_kernel<<<B, 128, 0, stream>>>(src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B);
+    check_launch();
+  }
+  // ---- phase 1: encoder ----
+  run_encoder(Mtok, B, max_src, d_off, d_len);
+  // ---- phase 2: Stage I (greedy; decoding.py:90-155 with beam = 1) ----
+  const int capA = max_cap + 1;  // start_cache(beam, max_steps + 1), decoding.py:97
+  {
+    Scope sc(this, K_OTHER, 0, 0);
+    stage1_init_kernel<<<cdiv(B, 128), 128, 0, stream>>>(B, capA, 4 + (k - 2) /*BOS_k*/, s_feed, s_done, s_nsteps,
+                                                        s_forced, s_score, s_hist);
+    check_launch();
+  }
+  CUDA_OK(cudaMemcpyAsync(s_caps, d_caps, B * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+  GreedyState gs{s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
+  for (int t = 0; t < max_cap; ++t) {
+    const int R = alive[t];
+    if (R == 0) break;
+    decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src);
+    vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
+    Scope sc(this, K_OTHER, 0, 0);
+    greedy_select_kernel<1><<<cdiv(R, 4), 128, 0, stream>>>(s1.parts, gs, R, t);
+    check_launch();
+  }
+  // ---- phase 3: Stage II over the greedy chain (b_nat = 1) ----
+  {
+    Scope sc(this, K_OTHER, 0, 0);
+    stage2_build_kernel<<<B, 128, 0, stream>>>(s_anchors, capA, d_seqmap, s_nsteps, d_off2, d_slot, B, k, s2.ids,
+                                               s2.pos, d_qlen2);
+    check_launch();
+  }
+  decoder_parallel(M2, B, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow);
+  vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
+  {
+    Scope sc(this, K_OTHER, 0, 0);
+    rowstat_kernel<1><<<cdiv(Mm, 4), 128, 0, stream>>>(s2.parts, Mm, 1, s2.mstat);
+    check_launch();
+  }
+  Stage2Out so;
+  so.tokens = on_device ? out->tokens : o_tokens;
+  so.lens = on_device ? out->lens : o_lens;
+  so.scores = on_device ? out->scores : o_scores;
+  so.calls = on_device ? out->calls : o_calls;
+  so.forced = on_device ? out->forced : o_forced;
+  so.out_index = d_perm;
+  {
+    Scope sc(this, K_OTHER, 0, 0);
+    stage2_finish_kernel<<<cdiv(B, 4), 128, 0, stream>>>(s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, d_seqmap,
+                                                        s_score, s_nsteps, s_forced, k, alpha, Lmax, B, so);
+    check_launch();
+  }
+  if (!on_device) {
+    CUDA_OK(cudaMemcpyAsync(out->tokens, o_tokens, (size_t)B * Lmax * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaMemcpyAsync(out->lens, o_lens, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaMemcpyAsync(out->scores, o_scores, B * 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaMemcpyAsync(out->calls, o_calls, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaMemcpyAsync(out->forced, o_forced, B, cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaStreamSynchronize(stream));
+    for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+  }
+  size_t hw = 0;
+  (void)hw;
+}
+
+}  // namespace hrt
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace hrt;
+
+struct hrt_engine {
+  std::unique_ptr<EngineBase> impl;
+};
+
+static std::string g_last_error;
+
+template <class Fn>
+static hrt_status guarded(hrt_engine* eng, Fn&& fn) {
+  try {
+    if (eng) cudaSetDevice(eng->impl->device);
+    fn();
+    return HRT_OK;
+  } catch (const HrtError& e) {
+    if (eng) eng->impl->last_error = e.what();
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (eng) eng->impl->last_error = e.what();
+    g_last_error = e.what();
+    return HRT_ERR_CUDA;
+  }
+}
+
+extern "C" {
+
+int64_t hrt_param_count(const hrt_config* cfg) { return Engine<float>::param_count(*cfg); }
+
+hrt_status hrt_create(const hrt_config* cfg, const float* params, int64_t n_params, int32_t device, hrt_engine** out) {
+  return guarded(nullptr, [&] {
+    if (!cfg || !params || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
+    if (n_params != Engine<float>::param_count(*cfg))
+      throw HrtError(HRT_ERR_INVALID, "n_params " + std::to_string(n_params) + " != expected " +
+                                          std::to_string(Engine<float>::param_count(*cfg)));
+    auto e = std::make_unique<hrt_engine>();
+    if (cfg->dtype == HRT_DTYPE_F32)
+      e->impl.reset(new Engine<float>(*cfg, params, device));
+    else if (cfg->dtype == HRT_DTYPE_BF16)
+      e->impl.reset(new Engine<bf16>(*cfg, params, device));
+    else
+      throw HrtError(HRT_ERR_INVALID, "unknown dtype");
+    *out = e.release();
+  });
+}
+
+void hrt_destroy(hrt_engine* eng) { delete eng; }
+
+const char* hrt_last_error(const hrt_engine* eng) {
+  return eng ? eng->impl->last_error.c_str() : g_last_error.c_str();
+}
+
+hrt_status hrt_get_stats(const hrt_engine* eng, hrt_stats* out) {
+  if (!eng || !out) return HRT_ERR_INVALID;
+  *out = eng->impl->stats;
+  return HRT_OK;
+}
+
+void* hrt_stream(hrt_engine* eng) { return eng ? (void*)eng->impl->stream : nullptr; }
+
+hrt_status hrt_synchronize(hrt_engine* eng) {
+  return guarded(eng, [&] { CUDA_OK(cudaStreamSynchronize(eng->impl->stream)); });
+}
+
+hrt_status hrt_encode(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t n_seq, float* memory_out) {
+  return guarded(eng, [&] { eng->impl->encode(ids, lens, n_seq, memory_out); });
+}
+
+hrt_status hrt_start_cache(hrt_engine* eng, int32_t rows, int32_t cap, const int32_t* row_seq) {
+  return guarded(eng, [&] { eng->impl->start_cache(rows, cap, row_seq); });
+}
+
+hrt_status hrt_step(hrt_engine* eng, const int32_t* tokens, int32_t position, float* logp_out) {
+  return guarded(eng, [&] { eng->impl->step(tokens, position, logp_out); });
+}
+
+hrt_status hrt_reorder(hrt_engine* eng, const int32_t* parents) {
+  return guarded(eng, [&] { eng->impl->reorder(parents); });
+}
+
+hrt_status hrt_parallel_logits(hrt_engine* eng, const int32_t* ids, const int32_t* positions, const uint8_t* pad_mask,
+                               int32_t B, int32_t T, int32_t mode, const int32_t* seq, float* logits_out) {
+  return guarded(eng, [&] { eng->impl->parallel_logits(ids, positions, pad_mask, B, T, mode, seq, logits_out); });
+}
+
+hrt_status hrt_argmax_logprobs(hrt_engine* eng, const int32_t* exclude, int32_t n_exclude, int32_t* amax_out,
+                               float* lp_out) {
+  return guarded(eng, [&] { eng->impl->argmax_logprobs(exclude, n_exclude, amax_out, lp_out); });
+}
+
+hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t B, int32_t k,
+                               int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
+                               const hrt_translate_out* out, int32_t io_on_device) {
+  return guarded(eng, [&] {
+    if (!ids || !lens || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
+    eng->impl->translate(ids, lens, B, k, b_at, b_nat, length_penalty, max_steps, out, io_on_device);
+  });
+}
+
+hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable) {
+  return guarded(eng, [&] {
+    EngineBase* e = eng->impl.get();
+    int cls = 0;
+    std::string c = kernel_class ? kernel_class : "all";
+    if (c == "vocab") cls = K_VOCAB;
+    else if (c == "gemm") cls = K_GEMM;
+    else if (c == "attn") cls = K_ATTN;
+    else if (c == "all") cls = K_GEMM | K_VOCAB | K_ATTN | K_OTHER;
+    else throw HrtError(HRT_ERR_INVALID, "unknown kernel class " + c);
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    e->timed_class = enable ? cls : 0;
+    e->ev_used = 0;
+    e->t_bytes = e->t_flops = 0;
+    e->t_launches = 0;
+  });
+}
+
+hrt_status hrt_timing_read(hrt_engine* eng, double* total_ms, int64_t* launches, double* alg_bytes,
+                           double* alg_flops) {
+  return guarded(eng, [&] {
+    EngineBase* e = eng->impl.get();
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    double ms = 0;
+    for (size_t i = 0; i < e->ev_used; ++i) {
+      float m = 0;
+      CUDA_OK(cudaEventElapsedTime(&m, e->ev_pool[i].first, e->ev_pool[i].second));
+      ms += m;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = e->t_launches;
+    if (alg_bytes) *alg_bytes = e->t_bytes;
+    if (alg_flops) *alg_flops = e->t_flops;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,296 @@
+"""Python face of the CUDA engine: `Engine` (fused batch path) and
+`CudaSession` (the reference's session protocol, infer.py:140-418).
+
+PyTorch is not needed here; host buffers are numpy arrays handed to the C ABI
+by pointer. `Engine.stream` exposes the engine's CUDA stream for callers that
+want to time on it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _lib
+from .model import EXCLUDED_OUTPUT_IDS, HRTModel, ModelConfig, ModelError, flat_params
+
+
+class InferenceError(RuntimeError):
+    """Reference infer.py:23."""
+
+
+class DecodingError(ValueError):
+    """Reference decoding.py:31."""
+
+
+class ArenaOverflowError(MemoryError):
+    """Reference arena.py:15 (device arena / capacity exceeded)."""
+
+
+class EngineCudaError(RuntimeError):
+    """CUDA runtime failure inside the engine."""
+
+
+_ERRORS = {
+    _lib.HRT_ERR_INVALID: ModelError,
+    _lib.HRT_ERR_INFERENCE: InferenceError,
+    _lib.HRT_ERR_DECODING: DecodingError,
+    _lib.HRT_ERR_MEMORY: ArenaOverflowError,
+    _lib.HRT_ERR_CUDA: EngineCudaError,
+}
+
+_DTYPES = {"float32": _lib.HRT_DTYPE_F32, "f32": _lib.HRT_DTYPE_F32, "fp32": _lib.HRT_DTYPE_F32,
+           "bfloat16": _lib.HRT_DTYPE_BF16, "bf16": _lib.HRT_DTYPE_BF16}
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _ptr(a, ctype=C.c_int32):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ctype))
+
+
+def _dtype_code(dtype):
+    if isinstance(dtype, str):
+        key = dtype.lower()
+    else:
+        key = np.dtype(dtype).name
+    if key not in _DTYPES:
+        raise ModelError(f"unsupported engine dtype {dtype!r} (float32 or bfloat16)")
+    return _DTYPES[key]
+
+
+class Engine:
+    """One device engine: weights, arena and KV caches live on `device`."""
+
+    def __init__(self, model, dtype="float32", device=0, max_sentences=1, max_beam=4, max_src_tokens=0,
+                 max_chunk=None):
+        self.lib = _lib.load()
+        self.config = ModelConfig.from_any(model.config)
+        c = self.config
+        self.dtype = "bfloat16" if _dtype_code(dtype) == _lib.HRT_DTYPE_BF16 else "float32"
+        self.cfg = _lib.HrtConfig(
+            c.d_model, c.d_ff, c.n_heads, c.enc_layers, c.dec_layers, c.vocab_size, c.max_len,
+            int(max_chunk or max(c.chunk_sizes)), _dtype_code(dtype), int(max_sentences), int(max_beam),
+            int(max_src_tokens))
+        blob = flat_params(model, np.float32)
+        n = self.lib.hrt_param_count(C.byref(self.cfg))
+        if n != blob.size:
+            raise ModelError(f"parameter count {blob.size} != engine layout {n}")
+        h = C.c_void_p()
+        self._h = None
+        self._check(self.lib.hrt_create(C.byref(self.cfg), _ptr(blob, C.c_float), n, int(device), C.byref(h)), None)
+        self._h = h
+        self.device = int(device)
+        self.max_sentences = int(max_sentences)
+        self.max_beam = int(max_beam)
+
+    # -- plumbing -----------------------------------------------------------
+    def _check(self, status, h="self"):
+        if status == _lib.HRT_OK:
+            return
+        handle = self._h if h == "self" else h
+        msg = self.lib.hrt_last_error(handle).decode(errors="replace")
+        raise _ERRORS.get(status, EngineCudaError)(msg)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.hrt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return self.lib.hrt_stream(self._h)
+
+    def synchronize(self):
+        self._check(self.lib.hrt_synchronize(self._h))
+
+    def stats(self):
+        s = _lib.HrtStats()
+        self._check(self.lib.hrt_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def timing_enable(self, kernel_class="all", enable=True):
+        self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
+
+    def timing_read(self):
+        ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        self._check(self.lib.hrt_timing_read(self._h, C.byref(ms), C.byref(n), C.byref(b), C.byref(f)))
+        return dict(ms=ms.value, launches=n.value, bytes=b.value, flops=f.value)
+
+    # -- fused batch path (decoding.hrt_translate for many sentences) --------
+    def translate_arrays(self, ids, lens, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None, out=None):
+        """Low-level call on packed host arrays; returns the output arrays."""
+        lens = _i32(lens)
+        B = int(lens.size)
+        ids = _i32(ids)
+        ms = None if max_steps is None else _i32(max_steps)
+        if out is None:
+            out = self.alloc_outputs(B)
+        o = _lib.HrtTranslateOut(out["tokens"].ctypes.data, out["lens"].ctypes.data, out["scores"].ctypes.data,
+                                 out["calls"].ctypes.data, out["forced"].ctypes.data)
+        self._check(self.lib.hrt_translate_batch(self._h, ids.ctypes.data, _ptr(lens), B, int(k), int(b_at),
+                                                 int(b_nat), float(length_penalty), _ptr(ms), C.byref(o), 0))
+        return out
+
+    def translate_device(self, ids_dev_ptr, lens, out_ptrs, k=2, b_at=1, b_nat=1, length_penalty=0.6,
+                         max_steps=None):
+        """Device-resident ids/outputs (raw CUDA pointers); lens/max_steps on host."""
+        lens = _i32(lens)
+        ms = None if max_steps is None else _i32(max_steps)
+        o = _lib.HrtTranslateOut(*out_ptrs)
+        self._check(self.lib.hrt_translate_batch(self._h, C.c_void_p(ids_dev_ptr), _ptr(lens), int(lens.size),
+                                                 int(k), int(b_at), int(b_nat), float(length_penalty), _ptr(ms),
+                                                 C.byref(o), 1))
+
+    def alloc_outputs(self, B, pinned=None):
+        L = self.config.max_len
+        mk = (lambda shape, dt: np.zeros(shape, dtype=dt)) if pinned is None else pinned
+        return dict(tokens=mk((B, L), np.int32), lens=mk((B,), np.int32), scores=mk((B, 3), np.float64),
+                    calls=mk((B,), np.int32), forced=mk((B,), np.uint8))
+
+    def translate_batch(self, sources, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None):
+        """List of Translation for a list of source id lists (one fused call)."""
+        from .decoding import Translation
+
+        t0 = time.perf_counter()
+        lens = np.array([len(s) for s in sources], dtype=np.int32)
+        ids = np.concatenate([np.asarray(s, dtype=np.int32) for s in sources]) if len(sources) else \
+            np.zeros(0, np.int32)
+        out = self.translate_arrays(ids, lens, k, b_at, b_nat, length_penalty, max_steps)
+        wall = time.perf_counter() - t0
+        res = []
+        for i in range(len(sources)):
+            n = int(out["lens"][i])
+            res.append(Translation(tokens=out["tokens"][i, :n].tolist(), skip_at_score=float(out["scores"][i, 0]),
+                                   skip_cmlm_score=float(out["scores"][i, 1]), score=float(out["scores"][i, 2]),
+                                   decoder_calls=int(out["calls"][i]), wall_time=wall, forced=bool(out["forced"][i])))
+        return res
+
+
+class DecoderCache:
+    """Handle for one in-flight causal decode (reference infer.py:109-124)."""
+
+    def __init__(self, beam, cap):
+        self.beam = beam
+        self.cap = cap
+        self.length = 0
+        self.last_position = None
+
+
+class CudaSession:
+    """Drop-in for `hrt.infer.InferenceSession` backed by the B200 engine.
+
+    Same methods and error behaviour; the Workspace/`ws` and `phase`
+    arguments are accepted for signature compatibility (the engine owns a
+    device arena sized in closed form at construction). Returned arrays are
+    fresh host copies, a superset of the reference's "valid until the next
+    call" contract.
+    """
+
+    def __init__(self, model, dtype=np.float32, device=0, max_sentences=1, max_beam=8, max_src_tokens=0):
+        if not hasattr(model, "params"):
+            raise ModelError("model must expose .config and .params")
+        self.engine = Engine(model, dtype=dtype, device=device, max_sentences=max_sentences, max_beam=max_beam,
+                             max_src_tokens=max_src_tokens)
+        self.config = self.engine.config
+        self.dtype = self.engine.dtype
+        self.decoder_calls = 0
+        self.src_len = 0
+        self._last_parallel = None
+
+    @classmethod
+    def random(cls, config, seed, dtype=np.float32, **kw):
+        return cls(HRTModel.random(config, seed), dtype=dtype, **kw)
+
+    # encode (infer.py:176-221)
+    def encode(self, src_ids, ws=None):
+        src = _i32(np.asarray(src_ids).reshape(-1))
+        s = int(src.size)
+        if s > self.config.max_len:
+            raise InferenceError(f"source length {s} exceeds max_len {self.config.max_len}")
+        mem = np.empty((s, self.config.d_model), dtype=np.float32)
+        lens = np.array([s], dtype=np.int32)
+        e = self.engine
+        e._check(e.lib.hrt_encode(e._h, _ptr(src), _ptr(lens), 1, _ptr(mem, C.c_float)))
+        self.src_len = s
+        self.memory = mem
+        return mem
+
+    # start_cache (infer.py:225-232)
+    def start_cache(self, beam, cache_cap, ws=None, phase="skip-at"):
+        e = self.engine
+        e._check(e.lib.hrt_start_cache(e._h, int(beam), int(cache_cap), None))
+        return DecoderCache(int(beam), int(cache_cap))
+
+    # step (infer.py:234-305)
+    def step(self, cache, tokens, position):
+        if cache.last_position is not None and position <= cache.last_position:
+            raise InferenceError("new position must exceed all cached positions")
+        if cache.length >= cache.cap:
+            raise InferenceError("decoder cache capacity exceeded")
+        toks = _i32(np.asarray(tokens).reshape(-1))
+        if toks.size != cache.beam:
+            raise InferenceError(f"expected {cache.beam} tokens, got {toks.size}")
+        out = np.empty((cache.beam, self.config.vocab_size), dtype=np.float32)
+        e = self.engine
+        e._check(e.lib.hrt_step(e._h, _ptr(toks), int(position), _ptr(out, C.c_float)))
+        cache.length += 1
+        cache.last_position = position
+        self.decoder_calls += 1
+        return out
+
+    # reorder (infer.py:307-318)
+    def reorder(self, cache, parents):
+        par = _i32(list(parents))
+        if par.size != cache.beam:
+            raise InferenceError("parents must name one row per beam")
+        e = self.engine
+        e._check(e.lib.hrt_reorder(e._h, _ptr(par)))
+
+    # parallel_logits (infer.py:322-399)
+    def parallel_logits(self, ids, positions, mode, ws=None, pad_mask=None, phase="skip-cmlm"):
+        ids = _i32(np.atleast_2d(np.asarray(ids)))
+        pos = _i32(np.atleast_2d(np.asarray(positions)))
+        if mode not in ("full", "causal"):
+            raise InferenceError(f"unknown mode {mode!r}")
+        B, T = ids.shape
+        pos = _i32(np.broadcast_to(pos, (B, T)))
+        pm = None
+        if pad_mask is not None:
+            pm = np.ascontiguousarray(np.asarray(pad_mask, dtype=bool).reshape(B, T), dtype=np.uint8)
+        out = np.empty((B, T, self.config.vocab_size), dtype=np.float32)
+        e = self.engine
+        e._check(e.lib.hrt_parallel_logits(e._h, _ptr(ids), _ptr(pos), _ptr(pm, C.c_uint8), B, T,
+                                           1 if mode == "causal" else 0, None, _ptr(out, C.c_float)))
+        self.decoder_calls += 1
+        self._last_parallel = (B, T)
+        return out
+
+    # argmax_logprobs (infer.py:401-418): computed on the device copy of the
+    # last parallel_logits; the passed array is not modified.
+    def argmax_logprobs(self, logits, exclude=None):
+        if self._last_parallel is None:
+            raise InferenceError("parallel_logits() must precede argmax_logprobs()")
+        B, T = self._last_parallel
+        ex = None if exclude is None else _i32(list(exclude))
+        amax = np.empty((B, T), dtype=np.int32)
+        lp = np.empty((B, T), dtype=np.float32)
+        e = self.engine
+        e._check(e.lib.hrt_argmax_logprobs(e._h, _ptr(ex), 0 if ex is None else int(ex.size), _ptr(amax),
+                                           _ptr(lp, C.c_float)))
+        return amax.astype(np.intp), lp
+
+    def translate_batch(self, sources, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None):
+        res = self.engine.translate_batch(sources, k, b_at, b_nat, length_penalty, max_steps)
+        self.decoder_calls += sum(t.decoder_calls for t in res)
+        return res
