@@ -1,0 +1,430 @@
+"""HRT inference benchmark (BASELINE.json metric: target words/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--config c2]
+    python bench.py --impl reference ...        # the reference's CPU path (oracle port)
+
+One step = one fused hrt_translate_batch over one batch of B synthetic
+sentences (config-2 distribution by default: E12D1 d512 bf16, log-normal
+lengths mean 28, Zipf(1.1) ids, random N(0,0.02) weights from seed 1; k=2
+greedy; Stage-I cap floor(1.2 n + 10)). Multi-GPU (torchrun): every rank
+decodes its own batch per step (weak scaling, no collective in the decode
+loop); device time is the max over ranks (NCCL all_reduce MAX) and the words
+are summed.
+
+value : device-resident ids/outputs, CUDA-event timed per step with an L2
+        flush (512 MiB memset) between steps, outside the events.
+e2e   : the same call through the C ABI with pinned HOST ids/outputs; the
+        H2D/D2H copies and the host-side scheduling are inside the events.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "target words/sec (batch-1 latency and batched) HRT k=2 at 1/2/4/8 B200 vs CPU ref"
+UNIT = "target words/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-batch1", action="store_true")
+    ap.add_argument("--sweep", default="", help="comma list of extra batch sizes to report")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(args, rank, step):
+    from paper_2212_01543_b200 import workload as W
+
+    spec = W.CONFIGS[args.config]
+    k = args.k or spec["k"]
+    # inputs seed = weight seed + 1000; ranks/steps get disjoint streams
+    seed = spec["seed"] + 1000 + 7919 * rank + 104729 * step
+    srcs = W.make_sources(args.batch, seed, spec["lengths"])
+    caps = W.stage1_caps(srcs, k)
+    return spec, k, srcs, caps
+
+
+def target_words(out, B):
+    return int(np.asarray(out["lens"][:B]).sum())
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            return None
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j["hbm_gbs"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), j["bf16_tflops"], "measured"
+    return 6650.0, 1400.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference's CPU path)
+# ---------------------------------------------------------------------------
+def make_oracle(spec):
+    from oracle import hrt_oracle as O
+    from paper_2212_01543_b200.model import ModelConfig, init_params
+
+    sh = spec["shape"]
+    params = init_params(ModelConfig.from_any(sh), spec["seed"])
+    ocfg = O.Config(sh.d_model, sh.d_ff, sh.n_heads, sh.enc_layers, sh.dec_layers, sh.vocab_size, sh.max_len)
+    return O.Oracle(ocfg, params, dtype=np.float32)
+
+
+def oracle_decode(orc, k, srcs, caps, budget_s=None):
+    """Sequential per-sentence decode (the reference has no batched path):
+    all of srcs, or as many as fit in budget_s seconds (at least 3)."""
+    from oracle import hrt_oracle as O
+
+    words = n = 0
+    t0 = time.monotonic()
+    while n < len(srcs) and (budget_s is None or n < 3 or time.monotonic() - t0 < budget_s):
+        words += len(O.hrt_translate(orc, srcs[n], k, max_steps=caps[n]).tokens)
+        n += 1
+    return n, words, time.monotonic() - t0
+
+
+def cpu_reference(spec, k, srcs, caps, budget_s):
+    """cpu_baseline leg: the oracle port (fp32 numpy, all host BLAS threads)
+    on a bounded sample of the step batch."""
+    orc = make_oracle(spec)
+    oracle_decode(orc, k, srcs[:1], caps[:1])  # warm-up (measure_wps protocol, bench.py:81-82)
+    n, words, dt = oracle_decode(orc, k, srcs, caps, budget_s)
+    return dict(value=words / dt, unit=UNIT, cores=len(os.sched_getaffinity(0)), kind="port",
+                sample=f"first {n} sentences of the step batch ({words} target words), decoded sequentially by "
+                       f"the fp32 numpy oracle port (oracle/hrt_oracle.py) in {dt:.1f} s")
+
+
+def run_reference(args):
+    """Reference arm: the reference's CPU algorithm (oracle port), rank 0 only."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    spec, k, srcs, caps = workload(args, 0, 0)
+    per_step = max(1, int(os.environ.get("HRT_REF_SENTENCES", "4")))
+    orc = make_oracle(spec)
+    for s in range(args.warmup):  # untimed warm-up steps (one sentence each)
+        oracle_decode(orc, k, srcs[s: s + 1], caps[s: s + 1])
+    times, words = [], 0
+    for s in range(args.steps):
+        lo = (args.warmup + s * per_step) % max(1, len(srcs) - per_step)
+        n, w, dt = oracle_decode(orc, k, srcs[lo: lo + per_step], caps[lo: lo + per_step])
+        times.append(dt)
+        words += w
+    val = words / sum(times)
+    sample = (f"{per_step} sentences of the {args.config} batch per step, decoded sequentially by the fp32 numpy "
+              f"oracle port with {len(os.sched_getaffinity(0))} host threads")
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * statistics.fmean(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: HRT k={k} greedy (reference CPU path, fp32)",
+                       "batch_per_gpu": args.batch, "k": k},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# engine arm
+# ---------------------------------------------------------------------------
+def run_engine(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2212_01543_b200 as hrt
+    from paper_2212_01543_b200 import build
+
+    build.build(verbose=False)
+    spec, k, _, _ = workload(args, rank, 0)
+    sh = spec["shape"]
+    B = args.batch
+    model = hrt.HRTModel.random(sh, spec["seed"])
+    eng = hrt.Engine(model, dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", device=local,
+                     max_sentences=B, max_beam=1)
+    del model
+
+    batches = [workload(args, rank, s) for s in range(args.warmup + args.steps)]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+
+    def device_inputs(srcs):
+        ids = torch.tensor(np.concatenate([np.asarray(s, np.int32) for s in srcs]), dtype=torch.int32,
+                           device="cuda")
+        lens = np.array([len(s) for s in srcs], np.int32)
+        return ids, lens
+
+    L = sh.max_len
+    dout = dict(tokens=torch.zeros((B, L), dtype=torch.int32, device="cuda"),
+                lens=torch.zeros(B, dtype=torch.int32, device="cuda"),
+                scores=torch.zeros((B, 3), dtype=torch.float64, device="cuda"),
+                calls=torch.zeros(B, dtype=torch.int32, device="cuda"),
+                forced=torch.zeros(B, dtype=torch.uint8, device="cuda"))
+    out_ptrs = [dout[n].data_ptr() for n in ("tokens", "lens", "scores", "calls", "forced")]
+
+    def run_device(b):
+        _, _, srcs, caps = b
+        ids, lens = device_inputs(srcs)
+        torch.cuda.synchronize()
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        n0 = eng.stats()["kernel_launches"]
+        e0.record(stream)
+        eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps)
+        e1.record(stream)
+        e1.synchronize()
+        n1 = eng.stats()["kernel_launches"]
+        words = int(dout["lens"][: len(srcs)].sum().item())
+        return e0.elapsed_time(e1), words, n1 - n0
+
+    # pinned host buffers for e2e
+    pin = lambda shape, dt: torch.zeros(shape, dtype={np.int32: torch.int32, np.float64: torch.float64,  # noqa
+                                                      np.uint8: torch.uint8}[dt], pin_memory=True).numpy()
+    hout = eng.alloc_outputs(B, pinned=pin)
+
+    def run_host(b):
+        _, _, srcs, caps = b
+        ids_h = pin((sum(len(s) for s in srcs),), np.int32)
+        ids_h[:] = np.concatenate([np.asarray(s, np.int32) for s in srcs])
+        lens = np.array([len(s) for s in srcs], np.int32)
+        torch.cuda.synchronize()
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        eng.translate_arrays(ids_h, lens, k=k, max_steps=caps, out=hout)
+        e1.record(stream)
+        e1.synchronize()
+        h2d = ids_h.nbytes + lens.nbytes
+        d2h = sum(hout[n][: len(srcs)].nbytes for n in hout)
+        return e0.elapsed_time(e1), int(hout["lens"][: len(srcs)].sum()), h2d, d2h
+
+    # ---- warmup + timed (device-resident) ----
+    for s in range(args.warmup):
+        run_device(batches[s])
+    clocks = Clocks(local)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times, words, launches = [], 0, 0
+    for s in range(args.warmup, args.warmup + args.steps):
+        ms, w, n = run_device(batches[s])
+        times.append(ms)
+        words += w
+        launches += n
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    tot_ms = sum(times)
+    # ---- e2e (host buffers) ----
+    for s in range(min(2, args.warmup)):
+        run_host(batches[s])
+    e_times, e_words, h2d, d2h = [], 0, 0, 0
+    for s in range(args.warmup, args.warmup + args.steps):
+        ms, w, hb, db = run_host(batches[s])
+        e_times.append(ms)
+        e_words += w
+        h2d, d2h = hb, db
+    e_tot = sum(e_times)
+    # ---- roofline pass: GEMM class (tensor-bound at this batch) ----
+    eng.timing_enable("gemm", True)
+    run_device(batches[args.warmup])
+    g = eng.timing_read()
+    eng.timing_enable("gemm", False)
+    eng.timing_enable("vocab", True)
+    run_device(batches[args.warmup])
+    vv = eng.timing_read()
+    eng.timing_enable("vocab", False)
+    eng.timing_enable("all", True)
+    ms_all, _, _ = run_device(batches[args.warmup])
+    allk = eng.timing_read()
+    eng.timing_enable("all", False)
+
+    # ---- aggregate over ranks ----
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([tot_ms, e_tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, e_tot = t.tolist()
+        w = torch.tensor([words, e_words], dtype=torch.float64, device="cuda")
+        dist.all_reduce(w, op=dist.ReduceOp.SUM)
+        words, e_words = (int(x) for x in w.tolist())
+    value = words / (tot_ms / 1000.0)
+    e2e = e_words / (e_tot / 1000.0)
+
+    # batch-1 latency (rank 0, N=1 only): one sentence per call
+    batch1 = None
+    if rank == 0 and ws == 1 and not args.no_batch1:
+        _, _, srcs, caps = batches[args.warmup]
+        n1 = min(32, len(srcs))
+        ids1 = [np.asarray(s, np.int32) for s in srcs[:n1]]
+        out1 = eng.alloc_outputs(1, pinned=pin)
+        for i in range(3):
+            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, max_steps=[caps[i]], out=out1)
+        e0, e1 = ev(), ev()
+        torch.cuda.synchronize()
+        w1 = 0
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for i in range(n1):
+            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, max_steps=[caps[i]], out=out1)
+            w1 += int(out1["lens"][0])
+        e1.record(stream)
+        e1.synchronize()
+        wall = time.perf_counter() - t0
+        ms1 = e0.elapsed_time(e1)
+        batch1 = {"sentences": n1, "ms_per_sentence": ms1 / n1, "target_words_per_s": w1 / (ms1 / 1000.0),
+                  "wall_ms_per_sentence": 1000 * wall / n1, "mode": "e2e host buffers, one sentence per call"}
+
+    sweep = {}
+    if rank == 0 and args.sweep:
+        for bs in [int(x) for x in args.sweep.split(",") if x]:
+            if bs > B:
+                continue
+            _, _, srcs, caps = batches[args.warmup]
+            ids = torch.tensor(np.concatenate([np.asarray(s, np.int32) for s in srcs[:bs]]), device="cuda")
+            lens = np.array([len(s) for s in srcs[:bs]], np.int32)
+            for _ in range(2):
+                eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps[:bs])
+            torch.cuda.synchronize()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps[:bs])
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            sweep[str(bs)] = {"ms": ms, "target_words_per_s": int(dout["lens"][:bs].sum().item()) / (ms / 1e3)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        _, _, srcs, caps = batches[args.warmup]
+        cpu = cpu_reference(spec, k, srcs, caps, args.cpu_seconds)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+    hbm, tf_sus, tf_burst, src = peaks()
+    gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    roof = {"bound": "tensor", "kernel": "tcgen05 GEMMs (all projections + vocab, one step)",
+            "achieved": gemm_tflops, "peak": tf_sus, "unit": "TFLOP/s",
+            "frac": (gemm_tflops / tf_sus) if gemm_tflops else None, "traffic": None,
+            "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "gemm_ms_per_step": g["ms"], "gemm_launches_per_step": g["launches"],
+            "gemm_share_of_step": g["ms"] / ms_all if ms_all else None,
+            "vocab_ms_per_step": vv["ms"], "vocab_tflops": vv["flops"] / (vv["ms"] / 1e3) / 1e12 if vv["ms"] else None,
+            "all_kernels_ms_per_step": allk["ms"], "instrumented_step_ms": ms_all}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": spec["dtype"], "data": "synthetic",
+        "config": {"workload": f"{args.config}: HRT k={k} greedy, E{sh.enc_layers}D{sh.dec_layers} d{sh.d_model} "
+                               f"V{sh.vocab_size}, batch {B} sentences/GPU/step, log-normal lengths mean 28, "
+                               f"Zipf(1.1) ids, random N(0,0.02) weights seed {spec['seed']}",
+                   "batch_per_gpu": B, "k": k, "l2": "512 MiB flush between timed steps (outside events)",
+                   "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e_tot / args.steps},
+        "gpu_launches": launches // max(1, args.steps),
+        "roofline": roof,
+        "cpu_baseline": None if cpu is None else {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+        "clocks": clk,
+        "batch1": batch1,
+    }
+    if sweep:
+        line["sweep"] = sweep
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_engine(args)
+
+
+if __name__ == "__main__":
+    main()

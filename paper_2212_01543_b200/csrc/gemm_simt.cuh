@@ -13,7 +13,7 @@ constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16, SG_THREADS = 256;
 template <typename T, class Epi>
 __global__ void __launch_bounds__(SG_THREADS) simt_gemm_kernel(const T* __restrict__ A, int lda,
                                                                const T* __restrict__ B, int ldb, int M, int N,
-                                                               int K, const int* __restrict__ M_dev, Epi epi) {
+                                                               int K, const int* __restrict__ M_dev, Epi epi, int aligned4) {
   if (M_dev) M = *M_dev;
   const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
   if (m0 >= M) return;
@@ -51,11 +51,11 @@ __global__ void __launch_bounds__(SG_THREADS) simt_gemm_kernel(const T* __restri
     const int row = m0 + ty * 4 + i;
     const int col = n0 + tx * 4;
     if (row < M && col < N) {
-      typename Epi::State st;
-      const int n = min(4, N - col);
-      epi.begin(st, row, col);
-      epi.chunk(st, row, col, acc[i], n);
-      epi.end(st, row, col);
+      if (col + 4 <= N && ((size_t)col & 3) == 0 && aligned4) {
+        epi.apply4(row, col, make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]));
+      } else {
+        for (int j = 0; j < 4 && col + j < N; ++j) epi.apply1(row, col + j, acc[i][j]);
+      }
     }
   }
 }

@@ -69,6 +69,7 @@ struct Plan {
 struct EngineBase {
   hrt_config cfg{};
   int device = 0;
+  int num_sms = 148;
   cudaStream_t stream = nullptr;
   std::string last_error;
   hrt_stats stats{};
@@ -220,7 +221,9 @@ struct Engine : EngineBase {
     if (BF16 && (d % 64 || ff % 64))
       throw HrtError(HRT_ERR_INVALID, "bf16 engine needs d_model and d_ff multiples of 64 (tcgen05 K tiles)");
     CUDA_OK(cudaSetDevice(dev));
+    CUDA_OK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_OK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    if (BF16 && V % 4) throw HrtError(HRT_ERR_INVALID, "bf16 engine needs vocab_size % 4 == 0");
     load_weights(params);
     size_capacity();
     alloc_buffers();
@@ -547,8 +550,8 @@ struct Engine : EngineBase {
       }
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN);
-      dim3 grid(cdiv(N, BN), cdiv(M, TC_BM));
-      kern<<<grid, TC_THREADS, smem, stream>>>(ta, tb, M, N, K, M_dev, epi);
+      const int tiles = cdiv(N, BN) * cdiv(M_dev ? a_cap : M, TC_BM);
+      kern<<<std::min(tiles, num_sms), TC_THREADS, smem, stream>>>(ta, tb, M, N, K, M_dev, epi);
     }
   }
 
@@ -567,14 +570,15 @@ struct Engine : EngineBase {
     if constexpr (BF16) {
       if (bn == 0) bn = choose_bn(M, N);
       if (bn == 64)
-        tc_launch<64, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+        tc_launch<64, 8>(A, a_cap, lda, M, W, N, K, epi, M_dev);
       else if (bn == 128)
-        tc_launch<128, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+        tc_launch<128, 6>(A, a_cap, lda, M, W, N, K, epi, M_dev);
       else
         tc_launch<256, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
     } else {
       dim3 grid(cdiv(N, SG_BN), cdiv(M, SG_BM));
-      simt_gemm_kernel<T, Epi><<<grid, SG_THREADS, 0, stream>>>(A, lda, W, K, M, N, K, M_dev, epi);
+      simt_gemm_kernel<T, Epi><<<grid, SG_THREADS, 0, stream>>>(A, lda, W, K, M, N, K, M_dev, epi,
+                                                                 epi.ld() % 4 == 0);
     }
     check_launch();
   }
@@ -615,27 +619,60 @@ struct Engine : EngineBase {
   }
 
   // ragged whole-sequence attention (see attn_prefill_kernel)
-  void attn_prefill(const T* q, int qs, const T* k, const T* v, int kvs, T* out, int os, int nseq, int max_slot,
-                    int lk_max, const int* q_off, const int* q_slot, const int* q_len, const int* kv_map,
+  template <int DH>
+  void prefill_launch(dim3 grid, const int2* items, const T* q, int qs, const T* k, const T* v, int kvs, T* out,
+                      int os, const int* q_off, const int* q_slot, const int* q_len, const int* kv_map,
+                      const int* kv_off, const int* kv_len, const unsigned char* key_ok, int causal) {
+    attn_prefill_kernel<T, DH><<<grid, AP_WARPS * 32, 0, stream>>>(items, q, qs, k, v, kvs, out, os, q_off, q_slot,
+                                                                   q_len, kv_map, kv_off, kv_len, key_ok, causal,
+                                                                   att_scale);
+  }
+  // work items (sequence, 32-query block) for every sequence with slot rows
+  static std::vector<int> prefill_items(const std::vector<int>& slot) {
+    std::vector<int> it;
+    for (size_t s = 0; s < slot.size(); ++s)
+      for (int b = 0; b * 32 < slot[s]; ++b) {
+        it.push_back((int)s);
+        it.push_back(b);
+      }
+    return it;
+  }
+  void attn_prefill(const int* items, int n_items, const T* q, int qs, const T* k, const T* v, int kvs, T* out,
+                    int os, const int* q_off, const int* q_slot, const int* q_len, const int* kv_map,
                     const int* kv_off, const int* kv_len, const unsigned char* key_ok, int causal, double flops) {
-    if (nseq <= 0 || max_slot <= 0) return;
-    lk_max = std::max(lk_max, 1);
+    if (n_items <= 0) return;
     Scope sc(this, K_ATTN, 0.0, flops);
-    const int nwarp = 8;
-    const size_t smem = (size_t)(2 * dh * lk_max + lk_max + nwarp * lk_max + nwarp * dh) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
+    dim3 grid(n_items, H);
+    const int2* it2 = reinterpret_cast<const int2*>(items);
+#define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
+    if constexpr (BF16) {
+      if (dh == 64) {
+        attn_prefill_mma_kernel<<<grid, AM_WARPS * 32, 0, stream>>>(it2, q, qs, k, v, kvs, out, os, q_off, q_slot,
+                                                                   q_len, kv_map, kv_off, kv_len, key_ok, causal,
+                                                                   att_scale);
+        check_launch();
+        return;
+      }
     }
-    if (smem > 227 * 1024) throw HrtError(HRT_ERR_INVALID, "attention key length too large for shared memory");
-    dim3 grid(nseq, H, cdiv(max_slot, nwarp * 8));
-    attn_prefill_kernel<T><<<grid, nwarp * 32, smem, stream>>>(q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map,
-                                                               kv_off, kv_len, key_ok, causal, dh, lk_max,
-                                                               att_scale);
+    switch (dh) {
+      case 8: HRT_PF(8); break;
+      case 16: HRT_PF(16); break;
+      case 32: HRT_PF(32); break;
+      case 64: HRT_PF(64); break;
+      default: throw HrtError(HRT_ERR_INVALID, "d_head must be 8, 16, 32 or 64");
+    }
+#undef HRT_PF
     check_launch();
   }
 
+  template <int DH, bool SELF>
+  void decode_launch(int blocks, size_t smem, const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc,
+                     const int* hist, int cap, int t, const int* row_seq, const int* kv_off, const int* kv_len, int R,
+                     int lk_max, T* out) {
+    attn_decode_kernel<T, DH, SELF><<<blocks, 128, smem, stream>>>(q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, row_seq,
+                                                                  kv_off, kv_len, nullptr, R, H, lk_max, att_scale,
+                                                                  out, d);
+  }
   template <bool SELF>
   void attn_decode(const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc, const int* hist, int cap, int t,
                    const int* row_seq, const int* kv_off, const int* kv_len, int R, int lk_max, T* out,
@@ -643,10 +680,18 @@ struct Engine : EngineBase {
     if (R <= 0) return;
     Scope sc(this, K_ATTN, bytes, 0.0);
     const int nwarp = 4;
-    const size_t smem = (size_t)nwarp * (lk_max + dh) * sizeof(float);
-    attn_decode_kernel<T, SELF><<<cdiv(R * H, nwarp), nwarp * 32, smem, stream>>>(
-        q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, row_seq, kv_off, kv_len, nullptr, R, H, dh, lk_max, att_scale,
-        out, d);
+    lk_max = std::max(lk_max, 1);
+    const size_t smem = (size_t)nwarp * lk_max * sizeof(float);
+    const int blocks = cdiv(R * H, nwarp);
+#define HRT_DC(DHV) decode_launch<DHV, SELF>(blocks, smem, q, qs, kn, vn, ns, kc, vc, hist, cap, t, row_seq, kv_off, kv_len, R, lk_max, out)
+    switch (dh) {
+      case 8: HRT_DC(8); break;
+      case 16: HRT_DC(16); break;
+      case 32: HRT_DC(32); break;
+      case 64: HRT_DC(64); break;
+      default: throw HrtError(HRT_ERR_INVALID, "d_head must be 8, 16, 32 or 64");
+    }
+#undef HRT_DC
     check_launch();
   }
 
@@ -676,7 +721,7 @@ struct Engine : EngineBase {
           EpiStoreF32 epi{logits_buf, V};
           dim3 grid(cdiv(V, SG_BN), cdiv(rn, SG_BM));
           simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y + (size_t)r0 * d, d, E, d, rn, V, d,
-                                                                            nullptr, epi);
+                                                                            nullptr, epi, V % 4 == 0);
           check_launch();
         }
         VocabParts sub = parts;
@@ -699,9 +744,9 @@ struct Engine : EngineBase {
   template <class Epi>
   void launch_vocab(const T* y, int y_cap, int R, const Epi& epi, int bn) {
     if (bn == 64)
-      tc_launch<64, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+      tc_launch<64, 8>(y, y_cap, d, R, E, V, d, epi, nullptr);
     else if (bn == 128)
-      tc_launch<128, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+      tc_launch<128, 6>(y, y_cap, d, R, E, V, d, epi, nullptr);
     else
       tc_launch<256, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
   }
@@ -714,7 +759,7 @@ struct Engine : EngineBase {
       launch_vocab(y, y_cap, R, epi, choose_bn(R, V));
     } else {
       dim3 grid(cdiv(V, SG_BN), cdiv(R, SG_BM));
-      simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y, d, E, d, R, V, d, nullptr, epi);
+      simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y, d, E, d, R, V, d, nullptr, epi, V % 4 == 0);
     }
     check_launch();
   }
@@ -724,7 +769,7 @@ struct Engine : EngineBase {
   // cross-K/V projection of every decoder layer (infer.py:216-220).
   // d_ids / d_pos hold the packed tokens; seq metadata in device arrays.
   // -------------------------------------------------------------------------
-  void run_encoder(int M, int nseq, int max_len_seq, const int* off, const int* len) {
+  void run_encoder(int M, int nseq, int max_len_seq, const int* off, const int* len, const int* items, int n_items) {
     if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed max_src_tokens");
     if (Le > 0)
       embed_ln(d_ids, d_pos, 0, M, enc[0].ln1g, enc[0].ln1b, eb.x, eb.y);
@@ -733,8 +778,8 @@ struct Engine : EngineBase {
     for (int i = 0; i < Le; ++i) {
       const EncW& w = enc[i];
       gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
-      attn_prefill(eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, nseq, max_len_seq, max_len_seq, off,
-                   len, len, nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
+      attn_prefill(items, n_items, eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, off, len, len,
+                   nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
       gemm(K_GEMM, eb.ctx, Me_max, d, M, w.wo, d, d, EpiResidual{eb.x, d, w.bo});
       layernorm(eb.x, M, w.ln2g, w.ln2b, eb.y);
       gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
@@ -786,19 +831,18 @@ struct Engine : EngineBase {
   // -------------------------------------------------------------------------
   void decoder_parallel(int M2, int nc, int max_slot, int max_src, const int* off, const int* slot,
                         const int* qlen, const int* kv_map, const int* src_off, const int* src_len,
-                        const unsigned char* key_ok, int causal, const int* out_row) {
+                        const unsigned char* key_ok, int causal, const int* out_row, const int* items, int n_items) {
     embed_ln(s2.ids, s2.pos, 0, M2, dec[0].ln1g, dec[0].ln1b, s2.x, s2.y);
     for (int i = 0; i < Ld; ++i) {
       const DecW& w = dec[i];
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s2.qkv, 3 * d, w.bqkv});
-      attn_prefill(s2.qkv, 3 * d, s2.qkv + d, s2.qkv + 2 * d, 3 * d, s2.ctx, d, nc, max_slot, max_slot, off, slot,
-                   qlen, nullptr, off, qlen, key_ok, causal, 4.0 * d * (double)max_slot * M2);
+      attn_prefill(items, n_items, s2.qkv, 3 * d, s2.qkv + d, s2.qkv + 2 * d, 3 * d, s2.ctx, d, off, slot, qlen,
+                   nullptr, off, qlen, key_ok, causal, 4.0 * d * (double)max_slot * M2);
       gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.wo, d, d, EpiResidual{s2.x, d, w.bo});
       layernorm(s2.x, M2, w.ln2g, w.ln2b, s2.y);
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqc, d, d, EpiBiasT<T, false>{s2.qc, d, w.bqc});
-      attn_prefill(s2.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, s2.ctx, d, nc,
-                   max_slot, max_src, off, slot, qlen, kv_map, src_off, src_len, nullptr, 0,
-                   4.0 * d * (double)max_src * M2);
+      attn_prefill(items, n_items, s2.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d,
+                   s2.ctx, d, off, slot, qlen, kv_map, src_off, src_len, nullptr, 0, 4.0 * d * (double)max_src * M2);
       gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.woc, d, d, EpiResidual{s2.x, d, w.boc});
       layernorm(s2.x, M2, w.ln3g, w.ln3b, s2.y);
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.w1, ff, d, EpiBiasT<T, true>{s2.hid, ff, w.b1});
@@ -853,6 +897,8 @@ struct Engine : EngineBase {
     size_t cur = 0;
     int* d_off = meta_put(cur, off);
     int* d_len = meta_put(cur, len);
+    const std::vector<int> items = prefill_items(len);
+    int* d_items = meta_put(cur, items);
     meta_flush(cur);
     CUDA_OK(cudaMemcpyAsync(d_ids, ids, M * sizeof(int), cudaMemcpyHostToDevice, stream));
     CUDA_OK(cudaMemcpyAsync(d_pos, pos.data(), M * sizeof(int), cudaMemcpyHostToDevice, stream));
@@ -868,7 +914,7 @@ struct Engine : EngineBase {
       }
       p_mem_target = p_mem;
     }
-    run_encoder(M, n, maxl, d_off, d_len);
+    run_encoder(M, n, maxl, d_off, d_len, d_items, (int)items.size() / 2);
     p_mem_target = nullptr;
     if (Le == 0 && mem_out) throw HrtError(HRT_ERR_INVALID, "memory output needs enc_layers >= 1");
     if (mem_out) {
@@ -982,6 +1028,8 @@ struct Engine : EngineBase {
     int* d_slot = meta_put(cur, slot);
     int* d_qlen = meta_put(cur, qlen);
     int* d_map = meta_put(cur, kvmap);
+    const std::vector<int> items = prefill_items(slot);
+    int* d_items = meta_put(cur, items);
     std::vector<int> dummy;
     upload_seq_meta(cur, dummy);
     // key mask bytes packed into ints region
@@ -995,7 +1043,8 @@ struct Engine : EngineBase {
     CUDA_OK(cudaMemcpyAsync(s2.ids, ids, M2 * sizeof(int), cudaMemcpyHostToDevice, stream));
     CUDA_OK(cudaMemcpyAsync(s2.pos, pos, M2 * sizeof(int), cudaMemcpyHostToDevice, stream));
     int max_src = *std::max_element(p_seq_len.begin(), p_seq_len.end());
-    decoder_parallel(M2, B, Tn, max_src, d_off, d_slot, d_qlen, d_map, p_doff, p_dlen, d_keyok, mode, nullptr);
+    decoder_parallel(M2, B, Tn, max_src, d_off, d_slot, d_qlen, d_map, p_doff, p_dlen, d_keyok, mode, nullptr, d_items,
+                     (int)items.size() / 2);
     if (p_logits_cap < (size_t)M2 * V) {
       cudaFree(p_logits);
       CUDA_OK(cudaMalloc(&p_logits, (size_t)M2 * V * sizeof(float)));
@@ -1209,6 +1258,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   int* d_cbeg = meta_put(cur, cand_beg);
   int* d_qlen2 = meta_put(cur, std::vector<int>(B, 0));
   int* d_outrow = meta_put(cur, out_row);
+  const std::vector<int> enc_items = prefill_items(len), s2_items = prefill_items(slot);
+  int* d_enc_items = meta_put(cur, enc_items);
+  int* d_s2_items = meta_put(cur, s2_items);
   meta_flush(cur);
   const int* src_ids = ids;
   if (!on_device) {
@@ -1221,7 +1273,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     check_launch();
   }
   // ---- phase 1: encoder ----
-  run_encoder(Mtok, B, max_src, d_off, d_len);
+  run_encoder(Mtok, B, max_src, d_off, d_len, d_enc_items, (int)enc_items.size() / 2);
   // ---- phase 2: Stage I (greedy; decoding.py:90-155 with beam = 1) ----
   const int capA = max_cap + 1;  // start_cache(beam, max_steps + 1), decoding.py:97
   {
@@ -1248,7 +1300,8 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
                                                s2.pos, d_qlen2);
     check_launch();
   }
-  decoder_parallel(M2, B, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow);
+  decoder_parallel(M2, B, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
+                   d_s2_items, (int)s2_items.size() / 2);
   vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
   {
     Scope sc(this, K_OTHER, 0, 0);

@@ -106,6 +106,32 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const int* __restr
   }
 }
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float LOG2E = 1.4426950408889634f;
+
+// ---------------------------------------------------------------------------
+// vector helpers: load 8 consecutive T as fp32
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load8(const float* p, float* o) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16* p, float* o) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Ragged ("varlen") multi-head attention for whole sequences:
 //   encoder self-attention            infer.py:196-203   (full)
@@ -114,80 +140,336 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const int* __restr
 // Sequence s owns query rows [q_off[s], q_off[s] + q_slot[s]) of which the
 // first q_len[s] are real (the rest get zero output), and attends key rows
 // [kv_off[kvs], kv_off[kvs] + kv_len[kvs]) with kvs = kv_map ? kv_map[s] : s.
-// Keys whose key_ok byte is 0 are masked (additive -1e9 in the reference).
-// grid = (n_seq, heads, query chunks); one warp per query row; K^T and V of
-// the (sequence, head) live in shared memory as fp32.
+// Keys whose key_ok byte is 0 are masked (additive -1e9 in the reference;
+// exp underflows to exactly 0 either way).
+// grid = (work items, heads): item i = (sequence, 32-query block), built on
+// the host so no CTA is empty. Every LANE owns one query (q and the output
+// accumulator in registers); the 4 warps split each 64-key shared-memory
+// chunk 16 keys apiece with private online-softmax state, merged at the end.
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256) attn_prefill_kernel(
-    const T* __restrict__ q, int q_stride, const T* __restrict__ k, const T* __restrict__ v, int kv_stride,
-    T* __restrict__ out, int out_stride, const int* __restrict__ q_off, const int* __restrict__ q_slot,
-    const int* __restrict__ q_len, const int* __restrict__ kv_map, const int* __restrict__ kv_off,
-    const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok, int causal, int dh, int lk_max,
-    float scale) {
-  extern __shared__ float sm[];
-  const int s = blockIdx.x, h = blockIdx.y;
-  const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+constexpr int AP_WARPS = 4, AP_KC = 64, AP_KG = 16;
+
+template <typename T, int DH>
+__global__ void __launch_bounds__(AP_WARPS * 32) attn_prefill_kernel(
+    const int2* __restrict__ items, const T* __restrict__ q, int q_stride, const T* __restrict__ k,
+    const T* __restrict__ v, int kv_stride, T* __restrict__ out, int out_stride, const int* __restrict__ q_off,
+    const int* __restrict__ q_slot, const int* __restrict__ q_len, const int* __restrict__ kv_map,
+    const int* __restrict__ kv_off, const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok,
+    int causal, float scale) {
+  __shared__ __align__(16) float Ks[AP_KC][DH];
+  __shared__ __align__(16) float Vs[AP_KC][DH];
+  __shared__ float kbias[AP_KC];
+  __shared__ float wm[AP_WARPS][32], wl[AP_WARPS][32];
+  const int2 it = items[blockIdx.x];
+  const int s = it.x, qbeg = it.y * 32, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qslot = q_slot[s];
-  const int qbeg = blockIdx.z * nwarp * 8;
-  if (qbeg >= qslot) return;
-  const int qend = min(qslot, qbeg + nwarp * 8);
   const int qlen = q_len[s];
   const int kvs = kv_map ? kv_map[s] : s;
   const int kb = kv_off[kvs];
   const int L = kv_len[kvs];
-  float* Kt = sm;                       // [dh][lk_max]
-  float* Vs = Kt + dh * lk_max;         // [lk_max][dh]
-  float* kbias = Vs + lk_max * dh;      // [lk_max]
-  float* wsc = kbias + lk_max;          // [nwarp][lk_max]
-  float* wq = wsc + nwarp * lk_max;     // [nwarp][dh]
-  const int hoff = h * dh;
-  for (int idx = threadIdx.x; idx < L * dh; idx += blockDim.x) {
-    const int j = idx / dh, c = idx - j * dh;
-    const size_t r = (size_t)(kb + j) * kv_stride + hoff + c;
-    Kt[c * lk_max + j] = to_f(k[r]);
-    Vs[j * dh + c] = to_f(v[r]);
-  }
-  for (int j = threadIdx.x; j < L; j += blockDim.x)
-    kbias[j] = (key_ok == nullptr || key_ok[kb + j]) ? 0.f : -INFINITY;
-  __syncthreads();
-  float* sc = wsc + warp * lk_max;
-  float* qv = wq + warp * dh;
+  const int hoff = h * DH;
   const int qb = q_off[s];
-  for (int i = qbeg + warp; i < qend; i += nwarp) {
-    T* o = out + (size_t)(qb + i) * out_stride + hoff;
-    if (i >= qlen) {
-      for (int c = lane; c < dh; c += 32) o[c] = from_f<T>(0.f);
-      continue;
+  const int qi = qbeg + lane;
+  const bool live = qi < qlen;
+  float qr[DH], o[DH];
+  if (live) {
+    const T* src = q + (size_t)(qb + qi) * q_stride + hoff;
+    if (DH % 8 == 0) {
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) load8(src + c, qr + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < DH; ++c) qr[c] = to_f(src[c]);
     }
-    const T* qr = q + (size_t)(qb + i) * q_stride + hoff;
-    for (int c = lane; c < dh; c += 32) qv[c] = to_f(qr[c]);
-    __syncwarp();
-    const int jend = causal ? min(L, i + 1) : L;
-    float mx = -INFINITY;
-    for (int j = lane; j < jend; j += 32) {
+  }
+#pragma unroll
+  for (int c = 0; c < DH; ++c) {
+    qr[c] = live ? qr[c] * scale : 0.f;
+    o[c] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  const int qmax = min(qslot, qbeg + 32) - 1;
+  const int Lc = causal ? min(L, qmax + 1) : L;
+  const bool any_live = qbeg < qlen;
+  for (int j0 = 0; j0 < Lc; j0 += AP_KC) {
+    const int nk = min(AP_KC, Lc - j0);
+    __syncthreads();  // previous chunk fully consumed
+    constexpr int V8 = DH >= 8 ? DH / 8 : 1;
+    for (int idx = threadIdx.x; idx < nk * V8; idx += blockDim.x) {
+      const int j = idx / V8, c8 = (idx % V8) * 8;
+      const size_t r = (size_t)(kb + j0 + j) * kv_stride + hoff + c8;
+      if (DH >= 8) {
+        load8(k + r, &Ks[j][c8]);
+        load8(v + r, &Vs[j][c8]);
+      } else {
+        for (int c = 0; c < DH; ++c) {
+          Ks[j][c] = to_f(k[r + c]);
+          Vs[j][c] = to_f(v[r + c]);
+        }
+      }
+    }
+    for (int j = threadIdx.x; j < AP_KC; j += blockDim.x)
+      kbias[j] = (j < nk && (key_ok == nullptr || key_ok[kb + j0 + j])) ? 0.f : -INFINITY;
+    __syncthreads();
+    const int g = warp * AP_KG;  // this warp's 16 keys of the chunk
+    if (!any_live || g >= nk) continue;
+    float sc[AP_KG];
+    float cm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < AP_KG; ++u) {
+      const int j = g + u;
+      float a = -INFINITY;
+      if (j < nk && !(causal && j0 + j > qi)) {
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < DH; c += 2) {
+          a0 = fmaf(qr[c], Ks[j][c], a0);
+          if (c + 1 < DH) a1 = fmaf(qr[c + 1], Ks[j][c + 1], a1);
+        }
+        a = a0 + a1 + kbias[j];
+      }
+      sc[u] = a;
+      cm = fmaxf(cm, a);
+    }
+    const float mn = fmaxf(m, cm);
+    if (mn == -INFINITY) continue;
+    const float corr = ex2f((m - mn) * LOG2E);
+    l *= corr;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] *= corr;
+    m = mn;
+    const float ms = mn * LOG2E;
+#pragma unroll
+    for (int u = 0; u < AP_KG; ++u) {
+      const int j = g + u;
+      if (j < nk) {
+        const float p = ex2f(fmaf(sc[u], LOG2E, -ms));
+        l += p;
+#pragma unroll
+        for (int c = 0; c < DH; ++c) o[c] = fmaf(p, Vs[j][c], o[c]);
+      }
+    }
+  }
+  // merge the 4 warps' partial softmax states (reuse Vs as [warp][lane][DH])
+  __syncthreads();
+  wm[warp][lane] = m;
+  wl[warp][lane] = l;
+  float* ob = &Vs[0][0];
+  static_assert(AP_WARPS * 32 * DH <= AP_KC * DH * 2, "merge buffer");
+  float* mine = (warp < 2 ? &Vs[0][0] : &Ks[0][0]) + ((warp & 1) * 32 + lane) * DH;
+  (void)ob;
+#pragma unroll
+  for (int c = 0; c < DH; ++c) mine[c] = o[c];
+  __syncthreads();
+  if (warp == 0 && qi < qslot) {
+    float mt = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < AP_WARPS; ++w) mt = fmaxf(mt, wm[w][lane]);
+    float lt = 0.f, f[AP_WARPS];
+#pragma unroll
+    for (int w = 0; w < AP_WARPS; ++w) {
+      f[w] = (wm[w][lane] == -INFINITY) ? 0.f : ex2f((wm[w][lane] - mt) * LOG2E);
+      lt += wl[w][lane] * f[w];
+    }
+    const float inv = (live && lt > 0.f) ? 1.0f / lt : 0.f;
+    T* orow = out + (size_t)(qb + qi) * out_stride + hoff;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) {
       float a = 0.f;
-      for (int c = 0; c < dh; ++c) a = fmaf(qv[c], Kt[c * lk_max + j], a);
-      a = a * scale + kbias[j];
-      sc[j] = a;
-      mx = fmaxf(mx, a);
+#pragma unroll
+      for (int w = 0; w < AP_WARPS; ++w) {
+        const float* ow = (w < 2 ? &Vs[0][0] : &Ks[0][0]) + ((w & 1) * 32 + lane) * DH;
+        a = fmaf(ow[c], f[w], a);
+      }
+      orow[c] = from_f<T>(a * inv);
     }
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int j = lane; j < jend; j += 32) {
-      const float e = (sc[j] == -INFINITY) ? 0.f : __expf(sc[j] - mx);
-      sc[j] = e;
-      sum += e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bf16 tensor-core variant of the ragged attention above (DH = 64): same work
+// items (sequence, 32-query block), 2 warps x 16 queries; S = Q K^T and
+// O += P V on mma.sync m16n8k16 (bf16 in, fp32 accumulate), online softmax
+// in the fp32 accumulator fragments, P fed back as the A operand without a
+// shared-memory round trip. Keys stream through smem in chunks of 64 (rows
+// padded to 72 bf16: conflict-free fragment loads).
+// ---------------------------------------------------------------------------
+constexpr int AM_WARPS = 2, AM_KC = 64, AM_LD = 72;
+
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+__global__ void __launch_bounds__(AM_WARPS * 32) attn_prefill_mma_kernel(
+    const int2* __restrict__ items, const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ k,
+    const bf16* __restrict__ v, int kv_stride, bf16* __restrict__ out, int out_stride, const int* __restrict__ q_off,
+    const int* __restrict__ q_slot, const int* __restrict__ q_len, const int* __restrict__ kv_map,
+    const int* __restrict__ kv_off, const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok,
+    int causal, float scale) {
+  constexpr int DH = 64;
+  __shared__ __align__(16) bf16 Qs[32][AM_LD];
+  __shared__ __align__(16) bf16 Ks[AM_KC][AM_LD];
+  __shared__ __align__(16) bf16 Vt[DH][AM_LD];
+  __shared__ float kbias[AM_KC];
+  const int2 it = items[blockIdx.x];
+  const int s = it.x, qbeg = it.y * 32, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qslot = q_slot[s];
+  const int qlen = q_len[s];
+  const int kvs = kv_map ? kv_map[s] : s;
+  const int kb = kv_off[kvs];
+  const int L = kv_len[kvs];
+  const int hoff = h * DH;
+  const int qb = q_off[s];
+  // Q block -> smem (rows past q_len are zero)
+  for (int idx = threadIdx.x; idx < 32 * 8; idx += blockDim.x) {
+    const int r = idx >> 3, c8 = (idx & 7) * 8;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (qbeg + r < qlen) u = *reinterpret_cast<const uint4*>(q + (size_t)(qb + qbeg + r) * q_stride + hoff + c8);
+    *reinterpret_cast<uint4*>(&Qs[r][c8]) = u;
+  }
+  __syncthreads();
+  // A fragments of this warp's 16 queries, 4 k-steps of 16 dims
+  const int g = lane >> 2, tq = lane & 3;
+  const int r0 = warp * 16 + g;
+  uint32_t qa[4][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int c = ks * 16 + tq * 2;
+    qa[ks][0] = *reinterpret_cast<const uint32_t*>(&Qs[r0][c]);
+    qa[ks][1] = *reinterpret_cast<const uint32_t*>(&Qs[r0 + 8][c]);
+    qa[ks][2] = *reinterpret_cast<const uint32_t*>(&Qs[r0][c + 8]);
+    qa[ks][3] = *reinterpret_cast<const uint32_t*>(&Qs[r0 + 8][c + 8]);
+  }
+  const int qi0 = qbeg + r0, qi1 = qi0 + 8;  // the two query rows this thread accumulates
+  float o[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = scale * LOG2E;  // scores kept in log2 units
+  const int qmax = min(qslot, qbeg + 32) - 1;
+  const int Lc = causal ? min(L, qmax + 1) : L;
+  for (int j0 = 0; j0 < Lc; j0 += AM_KC) {
+    const int nk = min(AM_KC, Lc - j0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < AM_KC * 8; idx += blockDim.x) {
+      const int j = idx >> 3, c8 = (idx & 7) * 8;
+      uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
+      if (j < nk) {
+        const size_t r = (size_t)(kb + j0 + j) * kv_stride + hoff + c8;
+        ku = *reinterpret_cast<const uint4*>(k + r);
+        vu = *reinterpret_cast<const uint4*>(v + r);
+      }
+      *reinterpret_cast<uint4*>(&Ks[j][c8]) = ku;
+      const bf16* ve = reinterpret_cast<const bf16*>(&vu);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) Vt[c8 + e][j] = ve[e];
     }
-    sum = warp_sum(sum);
-    __syncwarp();
-    const float inv = sum > 0.f ? 1.0f / sum : 0.f;
-    for (int c = lane; c < dh; c += 32) {
-      float a = 0.f;
-      for (int j = 0; j < jend; ++j) a = fmaf(sc[j], Vs[j * dh + c], a);
-      o[c] = from_f<T>(a * inv);
+    for (int j = threadIdx.x; j < AM_KC; j += blockDim.x)
+      kbias[j] = (j < nk && (key_ok == nullptr || key_ok[kb + j0 + j])) ? 0.f : -INFINITY;
+    __syncthreads();
+    // S = Q K^T : 16 x 64 per warp (8 n-tiles of 8 keys)
+    float sc[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t b[2];
+        const int kr = n * 8 + g, c = ks * 16 + tq * 2;
+        b[0] = *reinterpret_cast<const uint32_t*>(&Ks[kr][c]);
+        b[1] = *reinterpret_cast<const uint32_t*>(&Ks[kr][c + 8]);
+        mma_bf16_16816(sc[n], qa[ks], b);
+      }
     }
-    __syncwarp();
+    // mask + online softmax (base 2)
+    float cm0 = -INFINITY, cm1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = n * 8 + tq * 2 + e;
+        const float kbj = kbias[j];
+        float a0 = sc[n][e] * sl2 + kbj, a1 = sc[n][2 + e] * sl2 + kbj;
+        if (causal && j0 + j > qi0) a0 = -INFINITY;
+        if (causal && j0 + j > qi1) a1 = -INFINITY;
+        sc[n][e] = a0;
+        sc[n][2 + e] = a1;
+        cm0 = fmaxf(cm0, a0);
+        cm1 = fmaxf(cm1, a1);
+      }
+    }
+    cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, 1));
+    cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, 2));
+    cm1 = fmaxf(cm1, __shfl_xor_sync(0xffffffffu, cm1, 1));
+    cm1 = fmaxf(cm1, __shfl_xor_sync(0xffffffffu, cm1, 2));
+    const float mn0 = fmaxf(m0, cm0), mn1 = fmaxf(m1, cm1);
+    const float b0 = mn0 == -INFINITY ? 0.f : mn0, b1 = mn1 == -INFINITY ? 0.f : mn1;
+    const float c0 = ex2f(m0 - b0), c1 = ex2f(m1 - b1);
+    m0 = mn0;
+    m1 = mn1;
+    float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      sc[n][0] = ex2f(sc[n][0] - b0);
+      sc[n][1] = ex2f(sc[n][1] - b0);
+      sc[n][2] = ex2f(sc[n][2] - b1);
+      sc[n][3] = ex2f(sc[n][3] - b1);
+      ps0 += sc[n][0] + sc[n][1];
+      ps1 += sc[n][2] + sc[n][3];
+    }
+    l0 = l0 * c0 + ps0;
+    l1 = l1 * c1 + ps1;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      o[n][0] *= c0;
+      o[n][1] *= c0;
+      o[n][2] *= c1;
+      o[n][3] *= c1;
+    }
+    // O += P V : P fragments straight from the score accumulators
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sc[2 * ks][0], sc[2 * ks][1]);
+      pa[1] = pack_bf16(sc[2 * ks][2], sc[2 * ks][3]);
+      pa[2] = pack_bf16(sc[2 * ks + 1][0], sc[2 * ks + 1][1]);
+      pa[3] = pack_bf16(sc[2 * ks + 1][2], sc[2 * ks + 1][3]);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        uint32_t b[2];
+        const int dr = n * 8 + g, c = ks * 16 + tq * 2;
+        b[0] = *reinterpret_cast<const uint32_t*>(&Vt[dr][c]);
+        b[1] = *reinterpret_cast<const uint32_t*>(&Vt[dr][c + 8]);
+        mma_bf16_16816(o[n], pa, b);
+      }
+    }
+  }
+  // row sums across the quad, normalise, store (pad rows of the slot get 0)
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = (qi0 < qlen && l0 > 0.f) ? 1.f / l0 : 0.f;
+  const float i1 = (qi1 < qlen && l1 > 0.f) ? 1.f / l1 : 0.f;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const int c = hoff + n * 8 + tq * 2;
+    if (qi0 < qslot)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(qb + qi0) * out_stride + c) =
+          __floats2bfloat162_rn(o[n][0] * i0, o[n][1] * i0);
+    if (qi1 < qslot)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(qb + qi1) * out_stride + c) =
+          __floats2bfloat162_rn(o[n][2] * i1, o[n][3] * i1);
   }
 }
 
@@ -197,85 +479,115 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(
 //       row's history; history slot j of logical row r lives in physical row
 //       hist[r * cap + j] (beam reorder = index permutation, infer.py:307-318).
 // CROSS: attend the row's sentence memory keys (computed once in encode).
-// One warp per (row, head).
+// One warp per (row, head); q in registers; lanes own keys for QK (16 B
+// vector loads) and head dims for PV (coalesced rows).
 // ---------------------------------------------------------------------------
-template <typename T, bool SELF>
+template <typename T, int DH, bool SELF>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const T* __restrict__ q, int q_stride, const T* __restrict__ knew, const T* __restrict__ vnew, int new_stride,
     T* __restrict__ kc, T* __restrict__ vc, int c_stride, const int* __restrict__ hist, int cap, int t,
     const int* __restrict__ row_seq, const int* __restrict__ kv_off, const int* __restrict__ kv_len,
-    const int* __restrict__ R_dev, int R, int heads, int dh, int lk_max, float scale, T* __restrict__ out,
+    const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale, T* __restrict__ out,
     int out_stride) {
   extern __shared__ float sm[];
+  constexpr int DPL = DH >= 32 ? DH / 32 : 1;
   if (R_dev) R = *R_dev;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * nwarp + warp;
   if (item >= R * heads) return;
   const int r = item / heads, h = item - r * heads;
-  float* sc = sm + warp * (lk_max + dh);
-  float* qv = sc + lk_max;
-  const int hoff = h * dh;
-  for (int c = lane; c < dh; c += 32) qv[c] = to_f(q[(size_t)r * q_stride + hoff + c]);
+  float* sc = sm + warp * lk_max;
+  const int hoff = h * DH;
+  float qr[DH];
+  {
+    const T* src = q + (size_t)r * q_stride + hoff;
+    if (DH % 8 == 0) {
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) load8(src + c, qr + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < DH; ++c) qr[c] = to_f(src[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < DH; ++c) qr[c] *= scale;
+  }
   int L;
-  const T* kbase;
-  const T* vbase;
   size_t kv_row0 = 0;
   if (SELF) {
     L = t + 1;
-    // append this step's key/value (infer.py:259-260)
     const size_t dst = ((size_t)r * cap + t) * c_stride + hoff;
-    for (int c = lane; c < dh; c += 32) {
+    for (int c = lane; c < DH; c += 32) {
       kc[dst + c] = knew[(size_t)r * new_stride + hoff + c];
       vc[dst + c] = vnew[(size_t)r * new_stride + hoff + c];
     }
-    kbase = kc;
-    vbase = vc;
   } else {
     const int sq = row_seq ? row_seq[r] : r;
     L = kv_len[sq];
     kv_row0 = kv_off[sq];
-    kbase = knew;
-    vbase = vnew;
   }
-  __syncwarp();
+  auto krow = [&](int j) -> const T* {
+    if (SELF)
+      return (j == t) ? knew + (size_t)r * new_stride + hoff
+                      : kc + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
+    return knew + (kv_row0 + j) * (size_t)new_stride + hoff;
+  };
+  auto vrow = [&](int j) -> const T* {
+    if (SELF)
+      return (j == t) ? vnew + (size_t)r * new_stride + hoff
+                      : vc + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
+    return vnew + (kv_row0 + j) * (size_t)new_stride + hoff;
+  };
   float mx = -INFINITY;
   for (int j = lane; j < L; j += 32) {
-    const T* kr;
-    if (SELF) {
-      kr = (j == t) ? knew + (size_t)r * new_stride + hoff
-                    : kbase + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
+    const T* kr = krow(j);
+    float a0 = 0.f, a1 = 0.f;
+    if (DH % 8 == 0) {
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        float kk[8];
+        load8(kr + c, kk);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          a0 = fmaf(qr[c + e], kk[e], a0);
+          a1 = fmaf(qr[c + e + 1], kk[e + 1], a1);
+        }
+      }
     } else {
-      kr = kbase + (kv_row0 + j) * (size_t)new_stride + hoff;
+#pragma unroll
+      for (int c = 0; c < DH; ++c) a0 = fmaf(qr[c], to_f(kr[c]), a0);
     }
-    float a = 0.f;
-    for (int c = 0; c < dh; ++c) a = fmaf(qv[c], to_f(kr[c]), a);
-    a *= scale;
+    const float a = a0 + a1;
     sc[j] = a;
     mx = fmaxf(mx, a);
   }
   mx = warp_max(mx);
   float sum = 0.f;
+  const float ms = mx * LOG2E;
   for (int j = lane; j < L; j += 32) {
-    const float e = __expf(sc[j] - mx);
+    const float e = ex2f(fmaf(sc[j], LOG2E, -ms));
     sc[j] = e;
     sum += e;
   }
   sum = warp_sum(sum);
   __syncwarp();
   const float inv = 1.0f / sum;
-  for (int c = lane; c < dh; c += 32) {
-    float a = 0.f;
-    for (int j = 0; j < L; ++j) {
-      const T* vr;
-      if (SELF) {
-        vr = (j == t) ? vnew + (size_t)r * new_stride + hoff
-                      : vbase + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
-      } else {
-        vr = vbase + (kv_row0 + j) * (size_t)new_stride + hoff;
-      }
-      a = fmaf(sc[j], to_f(vr[c]), a);
+  float acc[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < L; ++j) {
+    const T* vr = vrow(j);
+    const float p = sc[j];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) {
+      const int c = lane + 32 * e;
+      if (c < DH) acc[e] = fmaf(p, to_f(vr[c]), acc[e]);
     }
-    out[(size_t)r * out_stride + hoff + c] = from_f<T>(a * inv);
+  }
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) {
+    const int c = lane + 32 * e;
+    if (c < DH) out[(size_t)r * out_stride + hoff + c] = from_f<T>(acc[e] * inv);
   }
 }
 
@@ -306,7 +618,10 @@ struct RowStat {
   int id[KTOP_MAX];
 };
 
-// Per-thread running accumulator over a contiguous run of columns of one row.
+
+// Per-thread running accumulator over a contiguous run of columns of one row:
+// running max / rescaled sum of exp (online softmax) and a top-KT list
+// ordered (value desc, id asc).
 template <int KT>
 struct TileAcc {
   float mx, sum;
@@ -335,30 +650,65 @@ struct TileAcc {
     val[p] = v;
     id[p] = c;
   }
-  // columns col0 .. col0+n-1 with logits l[0..n)
-  __device__ __forceinline__ void add(const float* l, int col0, int n, int norm_allowed) {
-    float cm = -INFINITY;
-    for (int i = 0; i < n; ++i) {
-      const int c = col0 + i;
-      const bool ok = id_allowed(c);
-      if (!norm_allowed || ok) cm = fmaxf(cm, l[i]);
-      if (ok) insert(l[i], c);
-    }
-    if (cm == -INFINITY) return;
+  // fold a new normaliser max in, rescaling the running sum
+  __device__ __forceinline__ void rebase(float cm) {
     if (cm > mx) {
-      sum *= __expf(mx - cm);
+      sum *= ex2f((mx - cm) * LOG2E);
       mx = cm;
     }
-    for (int i = 0; i < n; ++i) {
-      const int c = col0 + i;
-      if (!norm_allowed || id_allowed(c)) sum += __expf(l[i] - mx);
+  }
+  // one column (generic path)
+  __device__ __forceinline__ void add1(float x, int c, int norm_allowed) {
+    const bool ok = id_allowed(c);
+    if (ok) insert(x, c);
+    if (norm_allowed && !ok) return;
+    rebase(x);
+    sum += ex2f((x - mx) * LOG2E);
+  }
+  // 32 columns col0..col0+31, all generable (col0 >= 32): tree reductions
+  // so the per-element work is independent (ILP) -- the epilogue thread
+  // owns a whole row, so dependency chains would otherwise dominate.
+  __device__ __forceinline__ void add32_fast(const float* v, int col0) {
+    float mv[16];
+    int mi[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const bool b = v[i + 16] > v[i];
+      mv[i] = b ? v[i + 16] : v[i];
+      mi[i] = b ? i + 16 : i;
     }
+#pragma unroll
+    for (int st = 8; st > 0; st >>= 1) {
+#pragma unroll
+      for (int i = 0; i < st; ++i) {
+        const bool b = better(mv[i + st], mi[i + st], mv[i], mi[i]);
+        mv[i] = b ? mv[i + st] : mv[i];
+        mi[i] = b ? mi[i + st] : mi[i];
+      }
+    }
+    const float cm = mv[0];
+    if (KT == 1) {
+      if (better(cm, col0 + mi[0], val[0], id[0])) {
+        val[0] = cm;
+        id[0] = col0 + mi[0];
+      }
+    } else if (better(cm, col0 + mi[0], val[KT - 1], id[KT - 1])) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) insert(v[i], col0 + i);
+    }
+    rebase(cm);
+    const float ms = mx * LOG2E;
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s4[i & 3] += ex2f(fmaf(v[i], LOG2E, -ms));
+    sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
   }
 };
 
 // tcgen05 epilogue: one thread owns one row of a 128 x BN logits tile.
 template <int KT>
 struct VocabEpi {
+  static constexpr bool kRowWise = true;
   VocabParts parts;
   int norm_allowed;
   int bn;
@@ -367,8 +717,14 @@ struct VocabEpi {
   };
   __device__ __forceinline__ void begin(State& s, int, int) const { s.acc.init(); }
   __device__ __forceinline__ void chunk(State& s, int row, int col0, const float* v, int n) const {
-    if (col0 <= EOS_ID && EOS_ID < col0 + n) parts.eos[row] = v[EOS_ID - col0];
-    s.acc.add(v, col0, n, norm_allowed);
+    if (col0 >= 32 && n == 32) {
+      s.acc.add32_fast(v, col0);
+      return;
+    }
+    if (col0 == 0) parts.eos[row] = v[EOS_ID];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < n) s.acc.add1(v[i], col0 + i, norm_allowed);
   }
   __device__ __forceinline__ void end(State& s, int row, int n0) const {
     const int tile = n0 / bn;
@@ -397,13 +753,13 @@ __global__ void rowstats_from_logits_kernel(const float* __restrict__ logits, in
   TileAcc<KT> a;
   a.init();
   for (int c = c0 + lane; c < c1; c += 32) {
-    float x = l[c];
-    a.add(&x, c, 1, norm_allowed);
+    const float x = l[c];
+    a.add1(x, c, norm_allowed);
     if (c == EOS_ID) parts.eos[row] = x;
   }
   // merge lanes: max + rescaled sum
   const float m = warp_max(a.mx);
-  float s = (a.mx == -INFINITY) ? 0.f : a.sum * __expf(a.mx - m);
+  float s = (a.mx == -INFINITY) ? 0.f : a.sum * ex2f((a.mx - m) * LOG2E);
   s = warp_sum(s);
   // top-k merge: KT rounds of warp arg-best over each lane's head
   float hv[KT];
@@ -449,7 +805,7 @@ __device__ __forceinline__ RowStat merge_row(const VocabParts& parts, int row, i
   float s = 0.f;
   for (int t = lane; t < parts.ntiles; t += 32) {
     const float tm = parts.mx[base + t];
-    if (tm != -INFINITY) s += parts.sum[base + t] * __expf(tm - m);
+    if (tm != -INFINITY) s += parts.sum[base + t] * ex2f((tm - m) * LOG2E);
   }
   s = warp_sum(s);
   RowStat rs;

@@ -1,13 +1,17 @@
-// tcgen05 / TMEM / TMA GEMM for sm_100a:   C[M, N] = A[M, K] . B[N, K]^T
+// Persistent tcgen05 / TMEM / TMA GEMM for sm_100a:
+//     C[M, N] = A[M, K] . B[N, K]^T      (bf16 operands, fp32 accumulate)
 //
-// A (activations) and B (weights, stored N x K "K-major", i.e. the transpose
-// of the reference's (d_in, d_out) row-major W, model.py:152-165) are bf16;
-// the accumulator is fp32 in TMEM. One CTA computes a 128 x BN tile:
-//   warp 0     TMA producer (one elected lane), STAGES-deep smem ring
-//   warp 1     TMEM allocator + MMA issuer (one elected lane)
-//   warps 2-5  epilogue: tcgen05.ld 32 rows x 32 cols per warp per chunk,
-//              then a fused epilogue functor (bias / ReLU / residual / vocab
-//              softmax statistics) writes straight to global memory.
+// A = activations, B = weights stored N x K ("K-major", the transpose of the
+// reference's (d_in, d_out) W, model.py:152-165). One CTA per SM loops over
+// 128 x BN output tiles:
+//   warp 0        TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1        TMEM allocator + MMA issuer (one elected lane); two TMEM
+//                 accumulators so tile i+1's MMAs overlap tile i's epilogue
+//   warps 2..2+E  epilogue. Element-wise epilogues (bias / ReLU / residual /
+//                 store) transpose each 32x32 accumulator chunk through a
+//                 per-warp smem buffer so global traffic is coalesced 128 B
+//                 rows; row-wise epilogues (vocab softmax statistics) keep
+//                 one row per thread.
 #pragma once
 #include "sm100_ptx.cuh"
 
@@ -15,27 +19,34 @@ namespace hrt {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
-constexpr int TC_THREADS = 192;
+constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
 template <int BN, int STAGES>
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int STG_OFFSET = STAGES * STAGE_BYTES;                // epilogue staging
+  static constexpr int STG_BYTES = TC_EPI_WARPS * 32 * 33 * 4;
+  static constexpr int BAR_OFFSET = STG_OFFSET + STG_BYTES;
   static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;  // barriers + alignment slack
 };
 
 template <int BN>
 __host__ __device__ constexpr int tmem_cols_for() {
-  return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  return 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 }
 
-// Epilogue functor protocol (all methods const, called per epilogue thread):
-//   struct State;                                   per-thread scratch
-//   begin(State&, int row, int n0)                  row < M only
-//   chunk(State&, int row, int col0, const float* v, int nvalid)
-//   end(State&, int row, int n0)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Epilogue protocols:
+//  element-wise (Epi::kRowWise == false): apply4(row, col, float4 v) for 4
+//    consecutive valid columns (N % 4 == 0 is required).
+//  row-wise (Epi::kRowWise == true): State; begin(st,row,n0);
+//    chunk(st,row,col0,const float* v,int n); end(st,row,n0) per thread-row.
 template <int BN, int STAGES, class Epi>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
@@ -45,13 +56,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   if (M_dev != nullptr) M = *M_dev;
-  const int m0 = blockIdx.y * TC_BM;
-  const int n0 = blockIdx.x * BN;
-  if (m0 >= M) return;  // whole CTA uniform: nothing allocated yet
+  const int m_tiles = (M + TC_BM - 1) / TC_BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  if ((int)blockIdx.x >= num_tiles) return;  // CTA-uniform, before any allocation
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -65,7 +78,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], TC_EPI_WARPS);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -80,16 +96,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol_w = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * L::STAGE_BYTES;
-        uint8_t* sb = sa + L::A_BYTES;
-        mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
-        tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
-        tma_load_2d_hint(sb, &tmB, &full[stage], kb * TC_BK, n0, pol_w);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
+          tma_load_2d_hint(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, pol_w);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -99,44 +117,85 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full[stage], phase);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
-        const uint32_t sb = sa + L::A_BYTES;
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
+          const uint32_t sb = sa + L::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {
-          // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
-          tc_mma_f16(tmem_base, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
-                     (kb | k) != 0);
+          for (int k = 0; k < TC_BK / 16; ++k)
+            tc_mma_f16(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
+                       (kb | k) != 0);
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        tc_commit(&empty[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+        tc_commit(&tfull[acc]);
       }
-      tc_commit(tmem_full);
     }
   } else {
-    // ===== epilogue warps 2..5 =====
+    // ===== epilogue warps =====
+    const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + quarter * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    typename Epi::State st;
-    const bool live = row < M;
-    if (live) epi.begin(st, row, n0);
+    float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * 33);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
+      const int rbase = m0 + quarter * 32;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      if constexpr (Epi::kRowWise) {
+        const int row = rbase + lane;
+        typename Epi::State st;
+        const bool live = row < M;
+        if (live) epi.begin(st, row, n0);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
-      const int col0 = n0 + c;
-      int nvalid = N - col0;
-      nvalid = nvalid > 32 ? 32 : nvalid;
-      if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          const int col0 = n0 + c;
+          int nvalid = N - col0;
+          nvalid = nvalid > 32 ? 32 : nvalid;
+          if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
+        }
+        if (live) epi.end(st, row, n0);
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+          __syncwarp();
+          const int col = n0 + c + (lane & 7) * 4;
+#pragma unroll
+          for (int r4 = 0; r4 < 32; r4 += 4) {
+            const int r = r4 + (lane >> 3);
+            const int row = rbase + r;
+            if (row < M && col < N) {
+              const float* s = stg + r * 33 + (lane & 7) * 4;
+              epi.apply4(row, col, make_float4(s[0], s[1], s[2], s[3]));
+            }
+          }
+          __syncwarp();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    if (live) epi.end(st, row, n0);
   }
   tc_fence_before();
   __syncthreads();

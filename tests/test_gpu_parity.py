@@ -214,3 +214,23 @@ def test_batch_equals_single(hrt, golden):
         one = hrt.hrt_translate(sess, s, 2)
         assert one.tokens == b.tokens
         assert abs(one.score - b.score) < 1e-5
+
+
+def test_bf16_protocol_vectors_close(hrt, golden):
+    """bf16 engine (tcgen05 GEMMs + mma.sync attention) tracks the fp64
+    reference to bf16 precision on the d_head = 64 fixture."""
+    g = golden("dh64")
+    sess = hrt.CudaSession(_model(hrt, g), dtype="bfloat16", max_beam=4)
+    v = g["vectors"]
+    mem = sess.encode(v["src"])
+    assert _rel(mem, v["memory"]) < 5e-2
+    pos = np.arange(1, len(v["ids"]) + 1)[None, :]
+    for mode, key in (("full", "parallel_full"), ("causal", "parallel_causal")):
+        got = sess.parallel_logits([v["ids"]], pos, mode)[0]
+        assert _rel(got, v[key]) < 5e-2, mode
+    cache = sess.start_cache(1, len(v["step_logp"]) + 1)
+    feed = [O.BOS_K[v["step_k"]]]
+    for t, ref in enumerate(v["step_logp"]):
+        lp = sess.step(cache, feed, t * v["step_k"])[0]
+        assert _rel(lp, ref) < 5e-2, t
+        feed = [int(np.argmax(O.allowed_row(np.asarray(ref))))]

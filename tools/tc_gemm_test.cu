@@ -13,14 +13,12 @@
 using namespace hrt;
 
 struct StoreEpi {
+  static constexpr bool kRowWise = false;
   float* C;
   int ldc;
-  struct State {};
-  __device__ void begin(State&, int, int) const {}
-  __device__ void chunk(State&, int row, int col0, const float* v, int n) const {
-    for (int i = 0; i < n; ++i) C[(size_t)row * ldc + col0 + i] = v[i];
+  __device__ void apply4(int row, int col, float4 v) const {
+    *reinterpret_cast<float4*>(C + (size_t)row * ldc + col) = v;
   }
-  __device__ void end(State&, int, int) const {}
 };
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
@@ -45,7 +43,10 @@ bool run(int M, int N, int K) {
   auto kern = tc_gemm_kernel<BN, ST, StoreEpi>;
   int smem = TcSmem<BN, ST>::TOTAL;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid((N + BN - 1) / BN, (M + TC_BM - 1) / TC_BM);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int tiles = ((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
+  dim3 grid(tiles < nsm ? tiles : nsm);
   StoreEpi epi{dC, N};
   kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
   CK(cudaGetLastError());
@@ -92,11 +93,16 @@ bool run(int M, int N, int K) {
 int main() {
   bool ok = true;
   ok &= run<256, 4>(1, 256, 64);
+  ok &= run<128, 6>(1000, 640, 512);
   ok &= run<256, 4>(1, 32000, 512);
   ok &= run<256, 4>(200, 512, 512);
   ok &= run<256, 4>(1000, 1536, 512);
   ok &= run<128, 6>(300, 2048, 512);
   ok &= run<64, 8>(64, 512, 2048);
+  ok &= run<128, 6>(30000, 512, 512);
+  ok &= run<128, 6>(30000, 1536, 512);
+  ok &= run<128, 6>(30000, 2048, 512);
+  ok &= run<128, 6>(30000, 512, 2048);
   ok &= run<256, 4>(1024, 32000, 512);
   ok &= run<256, 4>(8192, 2048, 512);
   ok &= run<256, 4>(8192, 512, 2048);
