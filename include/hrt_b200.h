@@ -122,6 +122,10 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
                                int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
                                const hrt_translate_out* out, int32_t io_on_device);
 
+/* Engine options: "graphs" (1 = run the Stage-I loop as one captured CUDA
+ * graph with a conditional WHILE node, the default; 0 = launch step by step). */
+hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
+
 /* ---- measurement helpers ------------------------------------------------ */
 /* Kernel-class timing: when enabled, CUDA events bracket every launch of the
  * named class ("vocab", "gemm", "attn", "all") on the engine stream. */

@@ -94,6 +94,7 @@ struct EngineBase {
   virtual void parallel_logits(const int32_t* ids, const int32_t* pos, const uint8_t* pad, int B, int T, int mode,
                                const int32_t* seq, float* logits_out) = 0;
   virtual void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) = 0;
+  virtual void set_option(const std::string& name, int value) = 0;
   virtual void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
                          const int32_t* caps, const hrt_translate_out* out, int on_device) = 0;
 
@@ -159,12 +160,23 @@ struct Engine : EngineBase {
   // Stage-I state
   int *s_feed, *s_done, *s_nsteps, *s_forced, *s_anchors, *s_caps, *s_hist, *s_hist2, *s_rowseq, *s_parents;
   double* s_score;
+  StepCtl* s_ctl;
+  int *s_alive, *s_srcoff, *s_srclen;
+  // captured Stage-I loops (conditional WHILE graph), keyed by row bucket
+  struct LoopGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int kernels = 0;
+  };
+  std::map<int, LoopGraph> loop_graphs;
+  bool use_graphs = true;
   // outputs (device I/O staging)
   int *o_tokens, *o_lens, *o_calls;
   double* o_scores;
   unsigned char* o_forced;
   int* h_meta = nullptr;  // pinned staging for per-call metadata (one H2D copy)
   int meta_cap;
+  size_t meta_hdr = 0;     // ints reserved at the start for the fixed header
   cudaEvent_t meta_ev = nullptr;
 
   // ---- arena ----
@@ -239,6 +251,10 @@ struct Engine : EngineBase {
     cudaFree(p_logits);
     cudaFree(p_mem);
     if (h_meta) cudaFreeHost(h_meta);
+    for (auto& kv : loop_graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
     if (meta_ev) cudaEventDestroy(meta_ev);
   }
 
@@ -477,7 +493,7 @@ struct Engine : EngineBase {
 
   void alloc_buffers() {
     // persistent region
-    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256;
+    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256 + 8 + 2 * (cap_max + 8) + 2 * (Bmax + 16);
     auto persist_plan = [&](char* base) {
       Plan p;
       d_ids_raw = p.take<int>(base, Me_max + Bmax);
@@ -506,6 +522,13 @@ struct Engine : EngineBase {
     size_t pbytes = persist_plan(nullptr);
     CUDA_OK(cudaMalloc(&persist, pbytes));
     persist_plan(persist);
+    // fixed header of the metadata buffer: Stage-I loop control, alive[],
+    // source offsets / lengths (graph-captured kernels keep these pointers)
+    meta_hdr = 8 + align_up(cap_max + 1, 8) + align_up(Bmax + 1, 8) + align_up(Bmax, 8);
+    s_ctl = reinterpret_cast<StepCtl*>(d_meta);
+    s_alive = d_meta + 8;
+    s_srcoff = s_alive + align_up(cap_max + 1, 8);
+    s_srclen = s_srcoff + align_up(Bmax + 1, 8);
     arena_bytes = 0;
     for (int ph = 0; ph < 3; ++ph) {
       Plan p;
@@ -550,7 +573,7 @@ struct Engine : EngineBase {
       }
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN);
-      const int tiles = cdiv(N, BN) * cdiv(M_dev ? a_cap : M, TC_BM);
+      const int tiles = cdiv(N, BN) * cdiv(M, TC_BM);  // M: count, or upper bound with M_dev
       kern<<<std::min(tiles, num_sms), TC_THREADS, smem, stream>>>(ta, tb, M, N, K, M_dev, epi);
     }
   }
@@ -584,37 +607,46 @@ struct Engine : EngineBase {
   }
 
   template <int NPL>
-  void ln_launch(const float* x, int M, const float* g, const float* b, T* y, const int* out_row, float* y32) {
-    layernorm_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(x, nullptr, M, d, g, b, y, out_row, y32);
+  void ln_launch(const float* x, const int* M_dev, int M, const float* g, const float* b, T* y, const int* out_row,
+                 float* y32) {
+    layernorm_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(x, M_dev, M, d, g, b, y, out_row, y32);
   }
   void layernorm(const float* x, int M, const float* g, const float* b, T* y, const int* out_row = nullptr,
-                 float* y32 = nullptr) {
+                 float* y32 = nullptr, const int* M_dev = nullptr) {
     if (M <= 0) return;
     Scope sc(this, K_OTHER, (double)M * d * (4 + sizeof(T)), 8.0 * M * d);
     const int npl = cdiv(d, 32);
-    if (npl <= 1) ln_launch<1>(x, M, g, b, y, out_row, y32);
-    else if (npl <= 2) ln_launch<2>(x, M, g, b, y, out_row, y32);
-    else if (npl <= 4) ln_launch<4>(x, M, g, b, y, out_row, y32);
-    else if (npl <= 8) ln_launch<8>(x, M, g, b, y, out_row, y32);
-    else if (npl <= 16) ln_launch<16>(x, M, g, b, y, out_row, y32);
-    else ln_launch<32>(x, M, g, b, y, out_row, y32);
+#define HRT_LN(N) ln_launch<N>(x, M_dev, M, g, b, y, out_row, y32)
+    if (npl <= 1) HRT_LN(1);
+    else if (npl <= 2) HRT_LN(2);
+    else if (npl <= 4) HRT_LN(4);
+    else if (npl <= 8) HRT_LN(8);
+    else if (npl <= 16) HRT_LN(16);
+    else HRT_LN(32);
+#undef HRT_LN
     check_launch();
   }
 
   template <int NPL>
-  void emb_launch(const int* ids, const int* pos, int pc, int M, const float* g, const float* b, float* x, T* y) {
-    embed_ln_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(ids, pos, pc, nullptr, M, d, emb_scale, E, pe, g, b, x, y);
+  void emb_launch(const int* ids, const int* pos, int pc, const int* pos_dev, const int* M_dev, int M, const float* g,
+                  const float* b, float* x, T* y) {
+    embed_ln_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(ids, pos, pc, pos_dev, M_dev, M, d, emb_scale, E, pe, g, b,
+                                                            x, y);
   }
-  void embed_ln(const int* ids, const int* pos, int pos_const, int M, const float* g, const float* b, float* x, T* y) {
+  // M is the row count, or its upper bound when M_dev supplies it on device
+  void embed_ln(const int* ids, const int* pos, int pos_const, int M, const float* g, const float* b, float* x, T* y,
+                const int* pos_dev = nullptr, const int* M_dev = nullptr) {
     if (M <= 0) return;
     Scope sc(this, K_OTHER, (double)M * d * (4 + 4 + 2 * sizeof(T)), 8.0 * M * d);
     const int npl = cdiv(d, 32);
-    if (npl <= 1) emb_launch<1>(ids, pos, pos_const, M, g, b, x, y);
-    else if (npl <= 2) emb_launch<2>(ids, pos, pos_const, M, g, b, x, y);
-    else if (npl <= 4) emb_launch<4>(ids, pos, pos_const, M, g, b, x, y);
-    else if (npl <= 8) emb_launch<8>(ids, pos, pos_const, M, g, b, x, y);
-    else if (npl <= 16) emb_launch<16>(ids, pos, pos_const, M, g, b, x, y);
-    else emb_launch<32>(ids, pos, pos_const, M, g, b, x, y);
+#define HRT_EMB(N) emb_launch<N>(ids, pos, pos_const, pos_dev, M_dev, M, g, b, x, y)
+    if (npl <= 1) HRT_EMB(1);
+    else if (npl <= 2) HRT_EMB(2);
+    else if (npl <= 4) HRT_EMB(4);
+    else if (npl <= 8) HRT_EMB(8);
+    else if (npl <= 16) HRT_EMB(16);
+    else HRT_EMB(32);
+#undef HRT_EMB
     check_launch();
   }
 
@@ -667,23 +699,23 @@ struct Engine : EngineBase {
 
   template <int DH, bool SELF>
   void decode_launch(int blocks, size_t smem, const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc,
-                     const int* hist, int cap, int t, const int* row_seq, const int* kv_off, const int* kv_len, int R,
-                     int lk_max, T* out) {
-    attn_decode_kernel<T, DH, SELF><<<blocks, 128, smem, stream>>>(q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, row_seq,
-                                                                  kv_off, kv_len, nullptr, R, H, lk_max, att_scale,
-                                                                  out, d);
+                     const int* hist, int cap, int t, const int* t_dev, const int* row_seq, const int* kv_off,
+                     const int* kv_len, const int* R_dev, int R, int lk_max, T* out) {
+    attn_decode_kernel<T, DH, SELF><<<blocks, 128, smem, stream>>>(q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, t_dev,
+                                                                  row_seq, kv_off, kv_len, R_dev, R, H, lk_max,
+                                                                  att_scale, out, d);
   }
   template <bool SELF>
   void attn_decode(const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc, const int* hist, int cap, int t,
                    const int* row_seq, const int* kv_off, const int* kv_len, int R, int lk_max, T* out,
-                   double bytes) {
+                   double bytes, const int* t_dev = nullptr, const int* R_dev = nullptr) {
     if (R <= 0) return;
     Scope sc(this, K_ATTN, bytes, 0.0);
     const int nwarp = 4;
     lk_max = std::max(lk_max, 1);
     const size_t smem = (size_t)nwarp * lk_max * sizeof(float);
     const int blocks = cdiv(R * H, nwarp);
-#define HRT_DC(DHV) decode_launch<DHV, SELF>(blocks, smem, q, qs, kn, vn, ns, kc, vc, hist, cap, t, row_seq, kv_off, kv_len, R, lk_max, out)
+#define HRT_DC(DHV) decode_launch<DHV, SELF>(blocks, smem, q, qs, kn, vn, ns, kc, vc, hist, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, lk_max, out)
     switch (dh) {
       case 8: HRT_DC(8); break;
       case 16: HRT_DC(16); break;
@@ -696,7 +728,8 @@ struct Engine : EngineBase {
   }
 
   // vocab projection of R rows of y (K-major d) into tile partials.
-  void vocab_parts(const T* y, int y_cap, int R, VocabParts& parts, int kt, int norm_allowed, float* logits_buf) {
+  void vocab_parts(const T* y, int y_cap, int R, VocabParts& parts, int kt, int norm_allowed, float* logits_buf,
+                   const int* M_dev = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
       const int bn = choose_bn(R, V);
@@ -704,13 +737,14 @@ struct Engine : EngineBase {
       Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
       if (kt == 1) {
         VocabEpi<1> epi{parts, norm_allowed, bn};
-        launch_vocab(y, y_cap, R, epi, bn);
+        launch_vocab(y, y_cap, R, epi, bn, M_dev);
       } else {
         VocabEpi<KTOP_MAX> epi{parts, norm_allowed, bn};
-        launch_vocab(y, y_cap, R, epi, bn);
+        launch_vocab(y, y_cap, R, epi, bn, M_dev);
       }
       check_launch();
     } else {
+      if (M_dev) throw HrtError(HRT_ERR_INVALID, "device row count unsupported on the fp32 vocab path");
       // fp32: materialise logits in row blocks, then reduce per 256-col tile
       parts.ntiles = cdiv(V, 256);
       for (int r0 = 0; r0 < R; r0 += logit_rows) {
@@ -742,13 +776,13 @@ struct Engine : EngineBase {
     }
   }
   template <class Epi>
-  void launch_vocab(const T* y, int y_cap, int R, const Epi& epi, int bn) {
+  void launch_vocab(const T* y, int y_cap, int R, const Epi& epi, int bn, const int* M_dev = nullptr) {
     if (bn == 64)
-      tc_launch<64, 8>(y, y_cap, d, R, E, V, d, epi, nullptr);
+      tc_launch<64, 8>(y, y_cap, d, R, E, V, d, epi, M_dev);
     else if (bn == 128)
-      tc_launch<128, 6>(y, y_cap, d, R, E, V, d, epi, nullptr);
+      tc_launch<128, 6>(y, y_cap, d, R, E, V, d, epi, M_dev);
     else
-      tc_launch<256, 4>(y, y_cap, d, R, E, V, d, epi, nullptr);
+      tc_launch<256, 4>(y, y_cap, d, R, E, V, d, epi, M_dev);
   }
 
   // full fp32 logits of R rows (protocol face / parity), chunked
@@ -797,30 +831,34 @@ struct Engine : EngineBase {
   // one Stage-I decoder call for rows 0..R-1 at position `pos`, cache slot t
   // (infer.py:234-301 up to the final LN; vocab handled by the caller)
   // -------------------------------------------------------------------------
+  // ctl != nullptr: graph mode -- R is the upper bound (grid sizing) and the
+  // live row count, step and position are read from the device control block.
   void decoder_step(int R, int t, int pos, int cap, const int* feed, const int* hist, const int* row_seq,
-                    const int* kv_off, const int* kv_len, int max_src) {
-    embed_ln(feed, nullptr, pos, R, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
+                    const int* kv_off, const int* kv_len, int max_src, StepCtl* ctl = nullptr) {
+    const int* Rd = ctl ? &ctl->R : nullptr;
+    const int* td = ctl ? &ctl->t : nullptr;
+    embed_ln(feed, nullptr, pos, R, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, ctl ? &ctl->pos : nullptr, Rd);
     for (int i = 0; i < Ld; ++i) {
       const DecW& w = dec[i];
       T* kc = s1.kc + (size_t)i * R_max * cap_max * d;
       T* vc = s1.vc + (size_t)i * R_max * cap_max * d;
-      gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv});
+      gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv}, Rd);
       attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
-                        nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d);
-      gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo});
-      layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y);
-      gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc});
+                        nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd);
+      gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
+      layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y, nullptr, nullptr, Rd);
+      gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
       attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
                          nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
-                         2.0 * sizeof(T) * (double)R * max_src * d);
-      gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc});
-      layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y);
-      gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1});
-      gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2});
+                         2.0 * sizeof(T) * (double)R * max_src * d, nullptr, Rd);
+      gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
+      layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y, nullptr, nullptr, Rd);
+      gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
+      gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
       if (i + 1 < Ld)
-        layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y);
+        layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y, nullptr, nullptr, Rd);
       else
-        layernorm(s1.x, R, dec_lng, dec_lnb, s1.y);
+        layernorm(s1.x, R, dec_lng, dec_lnb, s1.y, nullptr, nullptr, Rd);
     }
   }
 
@@ -866,6 +904,7 @@ struct Engine : EngineBase {
     return d_meta + o;
   }
   void meta_flush(size_t cursor) {
+    // the fixed header (Stage-I control) is copied with the call's metadata
     CUDA_OK(cudaMemcpyAsync(d_meta, h_meta, cursor * sizeof(int), cudaMemcpyHostToDevice, stream));
     CUDA_OK(cudaEventRecord(meta_ev, stream));
   }
@@ -894,7 +933,7 @@ struct Engine : EngineBase {
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < len[i]; ++j) pos[off[i] + j] = j;
     meta_reset();
-    size_t cur = 0;
+    size_t cur = meta_hdr;
     int* d_off = meta_put(cur, off);
     int* d_len = meta_put(cur, len);
     const std::vector<int> items = prefill_items(len);
@@ -964,7 +1003,7 @@ struct Engine : EngineBase {
     for (int r = 0; r < p_rows; ++r)
       if (tokens[r] < 0 || tokens[r] >= V) throw HrtError(HRT_ERR_INVALID, "token id out of range");
     meta_reset();
-    size_t cur = 0;
+    size_t cur = meta_hdr;
     std::vector<int> dummy;
     upload_seq_meta(cur, dummy);
     meta_flush(cur);
@@ -1023,7 +1062,7 @@ struct Engine : EngineBase {
         kvmap[b] = seq[b];
       }
     meta_reset();
-    size_t cur = 0;
+    size_t cur = meta_hdr;
     int* d_off = meta_put(cur, off);
     int* d_slot = meta_put(cur, slot);
     int* d_qlen = meta_put(cur, qlen);
@@ -1059,7 +1098,52 @@ struct Engine : EngineBase {
     stats.decoder_calls += 1;
   }
 
+  // Capture (once per row bucket) the Stage-I step -- decoder layers, vocab
+  // statistics, greedy selection, loop advance -- as the body of a
+  // conditional WHILE node. Every step-varying value lives in s_ctl.
+  LoopGraph& loop_graph(int bucket, const GreedyState& gs) {
+    LoopGraph& lg = loop_graphs[bucket];
+    if (lg.exec) return lg;
+    CUDA_OK(cudaGraphCreate(&lg.graph, 0));
+    cudaGraphConditionalHandle h;
+    CUDA_OK(cudaGraphConditionalHandleCreate(&h, lg.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CUDA_OK(cudaGraphAddNode(&node, lg.graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int64_t before = stats.kernel_launches;
+    CUDA_OK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    try {
+      decoder_step(bucket, 0, 0, cap_max, s_feed, s_hist, nullptr, s_srcoff, s_srclen, Lmax, s_ctl);
+      vocab_parts(s1.y, R_max, bucket, s1.parts, 1, 0, s1.logits, &s_ctl->R);
+      greedy_select_kernel<1><<<cdiv(bucket, 4), 128, 0, stream>>>(s1.parts, gs, bucket, 0, s_ctl);
+      check_launch();
+      stage1_advance_kernel<<<1, 1, 0, stream>>>(s_ctl, s_alive, h);
+      check_launch();
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(stream, &dummy);
+      throw;
+    }
+    CUDA_OK(cudaStreamEndCapture(stream, &body));
+    lg.kernels = (int)(stats.kernel_launches - before) + 2;
+    stats.kernel_launches = before;
+    CUDA_OK(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+    return lg;
+  }
+
   void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) override;
+
+  void set_option(const std::string& name, int value) override {
+    if (name == "graphs")
+      use_graphs = value != 0;
+    else
+      throw HrtError(HRT_ERR_INVALID, "unknown option " + name);
+  }
 
   void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
                  const int32_t* caps, const hrt_translate_out* out, int on_device) override;
@@ -1162,7 +1246,7 @@ void Engine<T>::argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, 
   if (p_B == 0) throw HrtError(HRT_ERR_INFERENCE, "parallel_logits() must precede argmax_logprobs()");
   const int M2 = p_B * p_T;
   meta_reset();
-  size_t cur = 0;
+  size_t cur = meta_hdr;
   unsigned char* d_ex = nullptr;
   if (excl && n_excl > 0) {
     std::vector<unsigned char> m(V, 0);
@@ -1245,7 +1329,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   cand_beg[B] = B;
   meta_reset();
-  size_t cur = 0;
+  size_t cur = meta_hdr;
   int* d_rawoff = meta_put(cur, raw_off);
   int* d_perm = meta_put(cur, perm);
   int* d_off = meta_put(cur, off);
@@ -1261,6 +1345,16 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   const std::vector<int> enc_items = prefill_items(len), s2_items = prefill_items(slot);
   int* d_enc_items = meta_put(cur, enc_items);
   int* d_s2_items = meta_put(cur, s2_items);
+  {  // fixed header: loop control + alive[] + source offsets/lengths
+    StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, B, 0, 0};
+    std::memcpy(h_meta, &c, sizeof(StepCtl));
+    int* ha = h_meta + 8;
+    for (int t = 0; t <= cap_max; ++t) ha[t] = t < max_cap ? alive[t] : 0;
+    int* ho = ha + align_up(cap_max + 1, 8);
+    std::copy(off.begin(), off.end(), ho);
+    int* hl = ho + align_up(Bmax + 1, 8);
+    std::copy(len.begin(), len.end(), hl);
+  }
   meta_flush(cur);
   const int* src_ids = ids;
   if (!on_device) {
@@ -1275,7 +1369,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   // ---- phase 1: encoder ----
   run_encoder(Mtok, B, max_src, d_off, d_len, d_enc_items, (int)enc_items.size() / 2);
   // ---- phase 2: Stage I (greedy; decoding.py:90-155 with beam = 1) ----
-  const int capA = max_cap + 1;  // start_cache(beam, max_steps + 1), decoding.py:97
+  // cache capacity max_steps + 1 (start_cache, decoding.py:97); the fused path
+  // keeps the engine-wide stride cap_max so captured graphs stay valid
+  const int capA = cap_max;
   {
     Scope sc(this, K_OTHER, 0, 0);
     stage1_init_kernel<<<cdiv(B, 128), 128, 0, stream>>>(B, capA, 4 + (k - 2) /*BOS_k*/, s_feed, s_done, s_nsteps,
@@ -1284,14 +1380,24 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   CUDA_OK(cudaMemcpyAsync(s_caps, d_caps, B * sizeof(int), cudaMemcpyDeviceToDevice, stream));
   GreedyState gs{s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
-  for (int t = 0; t < max_cap; ++t) {
-    const int R = alive[t];
-    if (R == 0) break;
-    decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src);
-    vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
-    Scope sc(this, K_OTHER, 0, 0);
-    greedy_select_kernel<1><<<cdiv(R, 4), 128, 0, stream>>>(s1.parts, gs, R, t);
-    check_launch();
+  if (BF16 && use_graphs && timed_class == 0) {
+    // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
+    int bucket = 1;
+    while (bucket < B) bucket <<= 1;
+    bucket = std::min(bucket, R_max);
+    LoopGraph& lg = loop_graph(bucket, gs);
+    CUDA_OK(cudaGraphLaunch(lg.exec, stream));
+    stats.kernel_launches += (int64_t)lg.kernels * max_cap;
+  } else {
+    for (int t = 0; t < max_cap; ++t) {
+      const int R = alive[t];
+      if (R == 0) break;
+      decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src);
+      vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
+      Scope sc(this, K_OTHER, 0, 0);
+      greedy_select_kernel<1><<<cdiv(R, 4), 128, 0, stream>>>(s1.parts, gs, R, t, nullptr);
+      check_launch();
+    }
   }
   // ---- phase 3: Stage II over the greedy chain (b_nat = 1) ----
   {
@@ -1436,6 +1542,10 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
     if (!ids || !lens || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
     eng->impl->translate(ids, lens, B, k, b_at, b_nat, length_penalty, max_steps, out, io_on_device);
   });
+}
+
+hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value) {
+  return guarded(eng, [&] { eng->impl->set_option(name ? name : "", value); });
 }
 
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable) {

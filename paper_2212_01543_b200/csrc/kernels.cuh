@@ -19,7 +19,7 @@ constexpr int KTOP_MAX = 8;  // top-k width kept per vocab row (beam <= 7)
 // ---------------------------------------------------------------------------
 template <typename T, int NPL>
 __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restrict__ pos, int pos_const,
-                                const int* __restrict__ M_dev, int M, int d, float scale, const T* __restrict__ E,
+                                const int* __restrict__ pos_dev, const int* __restrict__ M_dev, int M, int d, float scale, const T* __restrict__ E,
                                 const float* __restrict__ pe, const float* __restrict__ g,
                                 const float* __restrict__ b, float* __restrict__ x, T* __restrict__ y) {
   if (M_dev) M = *M_dev;
@@ -27,7 +27,7 @@ __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restri
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const int id = ids[row];
-  const int p = pos ? pos[row] : pos_const;
+  const int p = pos ? pos[row] : (pos_dev ? *pos_dev : pos_const);
   float v[NPL];
   float s = 0.f;
 #pragma unroll
@@ -486,12 +486,13 @@ template <typename T, int DH, bool SELF>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const T* __restrict__ q, int q_stride, const T* __restrict__ knew, const T* __restrict__ vnew, int new_stride,
     T* __restrict__ kc, T* __restrict__ vc, int c_stride, const int* __restrict__ hist, int cap, int t,
-    const int* __restrict__ row_seq, const int* __restrict__ kv_off, const int* __restrict__ kv_len,
-    const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale, T* __restrict__ out,
-    int out_stride) {
+    const int* __restrict__ t_dev, const int* __restrict__ row_seq, const int* __restrict__ kv_off,
+    const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale,
+    T* __restrict__ out, int out_stride) {
   extern __shared__ float sm[];
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;
   if (R_dev) R = *R_dev;
+  if (t_dev) t = *t_dev;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * nwarp + warp;
   if (item >= R * heads) return;
@@ -857,6 +858,20 @@ __device__ __forceinline__ RowStat merge_row(const VocabParts& parts, int row, i
 //   score += fp32 log-softmax value of the token (full-vocab normaliser),
 //            accumulated in fp64.
 // ---------------------------------------------------------------------------
+// Device-side Stage-I loop control: the step kernels read the current step,
+// live-row count and position from here, so one captured step graph serves
+// every step (conditional WHILE node; stage1_advance_kernel steps it).
+struct StepCtl {
+  int t;         // current step
+  int R;         // rows alive at step t (prefix of the cap-sorted batch)
+  int pos;       // fed position t * k
+  int k;
+  int max_cap;   // steps to run at most
+  int nrows;     // rows in the batch
+  int finished;  // rows finished so far
+  int pad;
+};
+
 struct GreedyState {
   int* feed;       // [rows] next fed token
   int* done;       // [rows]
@@ -869,7 +884,11 @@ struct GreedyState {
 };
 
 template <int KT>
-__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t) {
+__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, StepCtl* ctl) {
+  if (ctl) {
+    R = ctl->R;
+    t = ctl->t;
+  }
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
@@ -887,7 +906,22 @@ __global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, in
     st.done[row] = 1;
     st.nsteps[row] = t + 1;
     st.forced[row] = last ? 1 : 0;
+    if (ctl) atomicAdd(&ctl->finished, 1);
   }
+}
+
+// End of one graph-resident Stage-I step: advance the control block and
+// decide whether the WHILE node runs another step (decoding.py:102, :149).
+__global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ alive,
+                                      cudaGraphConditionalHandle handle) {
+  const int t = ctl->t + 1;
+  const bool more = t < ctl->max_cap && ctl->finished < ctl->nrows && alive[t] > 0;
+  if (more) {
+    ctl->t = t;
+    ctl->R = alive[t];
+    ctl->pos = t * ctl->k;
+  }
+  cudaGraphSetConditional(handle, more ? 1u : 0u);
 }
 
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.

@@ -119,6 +119,10 @@ class Engine:
         self._check(self.lib.hrt_get_stats(self._h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in s._fields_}
 
+    def set_option(self, name, value):
+        """Engine option, e.g. set_option("graphs", 0) to launch Stage I step by step."""
+        self._check(self.lib.hrt_set_option(self._h, name.encode(), int(value)))
+
     def timing_enable(self, kernel_class="all", enable=True):
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 

@@ -234,3 +234,22 @@ def test_bf16_protocol_vectors_close(hrt, golden):
         lp = sess.step(cache, feed, t * v["step_k"])[0]
         assert _rel(lp, ref) < 5e-2, t
         feed = [int(np.argmax(O.allowed_row(np.asarray(ref))))]
+
+
+def test_graph_loop_equals_eager(hrt, golden):
+    """The captured Stage-I loop (conditional WHILE graph) reproduces the
+    step-by-step launch path exactly, for several batch buckets."""
+    g = golden("dh64")
+    eng = hrt.Engine(_model(hrt, g), dtype="bfloat16", max_sentences=64, max_beam=1)
+    from paper_2212_01543_b200 import workload as W
+
+    srcs = W.make_sources(37, 5, ("uniform", 3, 40), vocab_size=1000)
+    caps = W.stage1_caps(srcs, 2)
+    for n in (1, 5, 37):
+        eng.set_option("graphs", 1)
+        a = eng.translate_batch(srcs[:n], 2, max_steps=caps[:n])
+        eng.set_option("graphs", 0)
+        b = eng.translate_batch(srcs[:n], 2, max_steps=caps[:n])
+        for x, y in zip(a, b):
+            assert x.tokens == y.tokens
+            assert x.score == y.score and x.decoder_calls == y.decoder_calls
