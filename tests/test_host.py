@@ -1,0 +1,151 @@
+"""CPU-side checks: the C ABI library loads and exports every declared symbol,
+host logic (layout, init, workload, schedule) matches the oracle, and the
+product-side search/selection logic reproduces the oracle when it drives a
+numpy session (no GPU)."""
+
+import math
+import re
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_01543_b200 as hrt
+from paper_2212_01543_b200 import _lib, build, decoding as PD, workload as W
+from oracle import hrt_oracle as O
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    return build.build(verbose=False)
+
+
+def test_header_symbols_are_exported(lib_path):
+    hdr = open(os.path.join(REPO, "include", "hrt_b200.h")).read()
+    declared = set(re.findall(r"\b(hrt_[a-z_]+)\s*\(", hdr))
+    assert declared == set(_lib.EXPORTED)
+    assert set(_lib.exported_symbols(lib_path)) == declared
+
+
+def test_param_count_matches_layout(lib_path):
+    lib = _lib.load(lib_path)
+    import ctypes as C
+
+    for shape in (W.C1, W.C2, W.C4, hrt.ModelConfig(d_model=16, d_ff=64, n_heads=2, enc_layers=1, vocab_size=15,
+                                                   max_len=6)):
+        cfg = hrt.ModelConfig.from_any(shape)
+        c = _lib.HrtConfig(cfg.d_model, cfg.d_ff, cfg.n_heads, cfg.enc_layers, cfg.dec_layers, cfg.vocab_size,
+                           cfg.max_len, 4, 1, 1, 1, 0)
+        n = lib.hrt_param_count(C.byref(c))
+        assert n == sum(int(np.prod(s)) for _, s in hrt.param_layout(cfg))
+    # BASELINE parameter totals
+    assert sum(int(np.prod(s)) for _, s in hrt.param_layout(hrt.ModelConfig.from_any(W.C1))) == 39_504_384
+    assert sum(int(np.prod(s)) for _, s in hrt.param_layout(hrt.ModelConfig.from_any(W.C2))) == 58_418_688
+    assert sum(int(np.prod(s)) for _, s in hrt.param_layout(hrt.ModelConfig.from_any(W.C4))) == 217_520_128
+
+
+def test_layout_and_init_match_oracle():
+    cfg = hrt.ModelConfig(d_model=64, d_ff=128, n_heads=2, enc_layers=2, dec_layers=2, vocab_size=97, max_len=24)
+    ocfg = O.Config(64, 128, 2, 2, 2, 97, 24)
+    assert [(n, tuple(s)) for n, s in hrt.param_layout(cfg)] == [(n, tuple(s)) for n, s, _ in O.param_layout(ocfg)]
+    a, b = hrt.init_params(cfg, 3), O.init_params(ocfg, 3)
+    assert all(np.array_equal(a[k], b[k]) for k in a)
+
+
+def test_flat_params_order_and_shape_checks():
+    cfg = hrt.ModelConfig(d_model=16, d_ff=32, n_heads=2, enc_layers=1, vocab_size=15, max_len=6)
+    m = hrt.HRTModel.random(cfg, 1)
+    blob = hrt.model.flat_params(m)
+    assert blob.dtype == np.float32 and blob.size == sum(int(np.prod(s)) for _, s in hrt.param_layout(cfg))
+    assert np.array_equal(blob[: 15 * 16], m.params["embed"].astype(np.float32).reshape(-1))
+    bad = hrt.HRTModel(cfg, dict(m.params, embed=np.zeros((3, 3))))
+    with pytest.raises(hrt.ModelError):
+        hrt.model.flat_params(bad)
+
+
+def test_workload_generators():
+    a = W.make_sources(200, 1000, ("uniform", 8, 64))
+    b = W.make_sources(200, 1000, ("uniform", 8, 64))
+    assert a == b
+    for s in a:
+        assert s[-1] == W.EOS and 8 <= len(s) - 1 <= 64
+        assert all(4 <= t < 32000 for t in s[:-1])
+    ln = W.make_sources(4000, 1001, ("lognormal", 28.0, 0.5))
+    n = np.array([len(s) - 1 for s in ln])
+    assert n.min() >= 4 and n.max() <= 200 and 25 < n.mean() < 31
+    assert W.max_steps_for(36, 2) == math.ceil(math.floor(1.2 * 36 + 10) / 2) == O.max_steps_for(36, 2)
+
+
+def test_engine_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = hrt.ModelConfig(d_model=16, d_ff=32, n_heads=2, enc_layers=1, vocab_size=15, max_len=6)
+    with pytest.raises(hrt.EngineCudaError):
+        hrt.CudaSession(hrt.HRTModel.random(cfg, 1))
+
+
+def test_stage2_and_scoring_helpers():
+    s = PD.build_stage2_input([10, 11, 12, hrt.EOS], 2)
+    assert s.ids == [hrt.MASK, 10, hrt.MASK, 11, hrt.MASK, 12, hrt.MASK, hrt.EOS]
+    assert s.positions == list(range(1, 9))
+    with pytest.raises(hrt.DecodingError):
+        PD.build_stage2_input([10], 2)
+    h = PD.Hypothesis(tokens=[hrt.EOS], positions=[2], score=math.log(0.7), finished=True)
+    assert abs(PD.combined_score(h, [math.log(0.4)], 2) - (math.log(0.7) + math.log(0.4)) / 2 ** 0.6) < 1e-12
+    for bad in (hrt.MASK, hrt.PAD, hrt.EOS):
+        with pytest.raises(hrt.DecodingError):
+            PD.Translation([7, bad], 0.0, 0.0, 0.0, 1)
+    assert PD.truncate_at_eos([7, 8, hrt.EOS, 9]) == [7, 8]
+
+
+class OracleSession:
+    """The session protocol backed by the numpy oracle (test double): lets
+    the product-side host search run on CPU against the reference semantics."""
+
+    def __init__(self, orc):
+        self.o = orc
+        self.config = hrt.ModelConfig(orc.cfg.d_model, orc.cfg.d_ff, orc.cfg.n_heads, orc.cfg.enc_layers,
+                                      orc.cfg.dec_layers, orc.cfg.vocab_size, orc.cfg.max_len)
+        self.decoder_calls = 0
+
+    def encode(self, src, ws=None):
+        return self.o.encode(src)
+
+    def start_cache(self, beam, cap, ws=None, phase=None):
+        return self.o.start_cache(beam, cap)
+
+    def step(self, cache, tokens, position):
+        self.decoder_calls += 1
+        return self.o.step(cache, tokens, position)
+
+    def reorder(self, cache, parents):
+        self.o.reorder(cache, parents)
+
+    def parallel_logits(self, ids, positions, mode, ws=None, pad_mask=None, phase=None):
+        self.decoder_calls += 1
+        return self.o.parallel_logits(ids, positions, mode, pad_mask)
+
+    def argmax_logprobs(self, logits, exclude=None):
+        return self.o.argmax_logprobs(logits, exclude)
+
+
+@pytest.mark.parametrize("name", ["tiny_trained", "toy"])
+def test_product_search_matches_golden_on_cpu(golden, name):
+    g = golden(name)
+    c = g["config"]
+    ocfg = O.Config(**{k: (tuple(v) if k == "chunk_sizes" else v) for k, v in c.items()})
+    params = ({k: np.asarray(v) for k, v in g["params"].items()} if "params" in g else O.init_params(ocfg, g["seed"]))
+    sess = OracleSession(O.Oracle(ocfg, params, np.float64))
+    for r in g["runs"][::3]:
+        tr = PD.hrt_translate(sess, g["sources"][r["src"]], r["k"], r["b_at"], r["b_nat"], max_steps=r["max_steps"])
+        assert tr.tokens == r["out"]["tokens"]
+        assert abs(tr.score - r["out"]["score"]) < 1e-9
+        assert tr.decoder_calls == r["out"]["decoder_calls"] and tr.forced == r["out"]["forced"]
+    if name == "tiny_trained":
+        for r in g["at_runs"]:
+            tr = PD.at_translate(sess, g["sources"][r["src"]], beam=r["beam"])
+            assert tr.tokens == r["out"]["tokens"] and abs(tr.score - r["out"]["score"]) < 1e-9
