@@ -246,6 +246,8 @@ def run_engine(args):
                 forced=torch.zeros(B, dtype=torch.uint8, device="cuda"))
     out_ptrs = [dout[n].data_ptr() for n in ("tokens", "lens", "scores", "calls", "forced")]
 
+    phases = []
+
     def run_device(b):
         _, _, srcs, caps = b
         ids, lens = device_inputs(srcs)
@@ -259,6 +261,7 @@ def run_engine(args):
         e1.record(stream)
         e1.synchronize()
         n1 = eng.stats()["kernel_launches"]
+        phases.append(eng.phase_times())
         words = int(dout["lens"][: len(srcs)].sum().item())
         return e0.elapsed_time(e1), words, n1 - n0
 
@@ -293,6 +296,7 @@ def run_engine(args):
     torch.cuda.synchronize()
     clocks.start()
     times, words, launches = [], 0, 0
+    phases.clear()
     for s in range(args.warmup, args.warmup + args.steps):
         ms, w, n = run_device(batches[s])
         times.append(ms)
@@ -301,6 +305,8 @@ def run_engine(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     tot_ms = sum(times)
+    phase_ms = {key: statistics.fmean(p[key] for p in phases) for key in ("encoder", "stage1", "stage2")}
+    stage1_steps = statistics.fmean(max(b[3]) for b in batches[args.warmup:])
     # ---- e2e (host buffers) ----
     for s in range(min(2, args.warmup)):
         run_host(batches[s])
@@ -412,6 +418,7 @@ def run_engine(args):
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e_tot / args.steps},
         "gpu_launches": launches // max(1, args.steps),
+        "phase_ms_per_step": phase_ms, "stage1_steps_per_step": stage1_steps,
         "roofline": roof,
         "cpu_baseline": None if cpu is None else {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
         "clocks": clk,

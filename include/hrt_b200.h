@@ -130,6 +130,9 @@ hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
 /* Kernel-class timing: when enabled, CUDA events bracket every launch of the
  * named class ("vocab", "gemm", "attn", "all") on the engine stream. */
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable);
+/* Device milliseconds of the last hrt_translate_batch's phases:
+ * ms3[0] encoder (+cross-K/V), ms3[1] Stage I loop, ms3[2] Stage II + selection. */
+hrt_status hrt_phase_times(hrt_engine* eng, float* ms3);
 /* Total device milliseconds and launch count of the timed class since enable. */
 hrt_status hrt_timing_read(hrt_engine* eng, double* total_ms, int64_t* launches, double* alg_bytes,
                            double* alg_flops);

@@ -41,6 +41,27 @@ struct EpiBiasT {
     }
     store4(out + (size_t)row * ldo + col, v);
   }
+  __device__ __forceinline__ void apply8(int row0, int col, const float4* v, int M) const {
+    const float4 b = *reinterpret_cast<const float4*>(bias + col);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = row0 + 4 * i;
+      if (row < M) {
+        float4 a = v[i];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+        if (RELU) {
+          a.x = fmaxf(a.x, 0.f);
+          a.y = fmaxf(a.y, 0.f);
+          a.z = fmaxf(a.z, 0.f);
+          a.w = fmaxf(a.w, 0.f);
+        }
+        store4(out + (size_t)row * ldo + col, a);
+      }
+    }
+  }
   __device__ __forceinline__ void apply1(int row, int col, float v) const {
     float a = v + bias[col];
     if (RELU) a = fmaxf(a, 0.f);
@@ -64,6 +85,24 @@ struct EpiResidual {
     a.w += v.w + b.w;
     *reinterpret_cast<float4*>(p) = a;
   }
+  __device__ __forceinline__ void apply8(int row0, int col, const float4* v, int M) const {
+    const float4 b = *reinterpret_cast<const float4*>(bias + col);
+    float4 prev[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (row0 + 4 * i < M) prev[i] = *reinterpret_cast<const float4*>(x + (size_t)(row0 + 4 * i) * ldx + col);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (row0 + 4 * i < M) {
+        float4 a = prev[i];
+        a.x += v[i].x + b.x;
+        a.y += v[i].y + b.y;
+        a.z += v[i].z + b.z;
+        a.w += v[i].w + b.w;
+        *reinterpret_cast<float4*>(x + (size_t)(row0 + 4 * i) * ldx + col) = a;
+      }
+    }
+  }
   __device__ __forceinline__ void apply1(int row, int col, float v) const {
     x[(size_t)row * ldx + col] += v + bias[col];
   }
@@ -76,6 +115,11 @@ struct EpiStoreF32 {
   __host__ __device__ int ld() const { return ldo; }
   __device__ __forceinline__ void apply4(int row, int col, float4 v) const {
     store4(out + (size_t)row * ldo + col, v);
+  }
+  __device__ __forceinline__ void apply8(int row0, int col, const float4* v, int M) const {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (row0 + 4 * i < M) store4(out + (size_t)(row0 + 4 * i) * ldo + col, v[i]);
   }
   __device__ __forceinline__ void apply1(int row, int col, float v) const { out[(size_t)row * ldo + col] = v; }
 };

@@ -73,6 +73,13 @@ struct EngineBase {
   cudaStream_t stream = nullptr;
   std::string last_error;
   hrt_stats stats{};
+  // phase timing: events at the phase boundaries of the last fused call
+  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool phase_valid = false;
+  void phase_mark(int i) {
+    if (!phase_ev[i]) cudaEventCreate(&phase_ev[i]);
+    cudaEventRecord(phase_ev[i], stream);
+  }
   // kernel-class timing
   int timed_class = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -1367,7 +1374,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     check_launch();
   }
   // ---- phase 1: encoder ----
+  phase_mark(0);
   run_encoder(Mtok, B, max_src, d_off, d_len, d_enc_items, (int)enc_items.size() / 2);
+  phase_mark(1);
   // ---- phase 2: Stage I (greedy; decoding.py:90-155 with beam = 1) ----
   // cache capacity max_steps + 1 (start_cache, decoding.py:97); the fused path
   // keeps the engine-wide stride cap_max so captured graphs stay valid
@@ -1399,6 +1408,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
       check_launch();
     }
   }
+  phase_mark(2);
   // ---- phase 3: Stage II over the greedy chain (b_nat = 1) ----
   {
     Scope sc(this, K_OTHER, 0, 0);
@@ -1427,6 +1437,8 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
                                                         s_score, s_nsteps, s_forced, k, alpha, Lmax, B, so);
     check_launch();
   }
+  phase_mark(3);
+  phase_valid = true;
   if (!on_device) {
     CUDA_OK(cudaMemcpyAsync(out->tokens, o_tokens, (size_t)B * Lmax * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->lens, o_lens, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -1546,6 +1558,15 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
 
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value) {
   return guarded(eng, [&] { eng->impl->set_option(name ? name : "", value); });
+}
+
+hrt_status hrt_phase_times(hrt_engine* eng, float* ms3) {
+  return guarded(eng, [&] {
+    EngineBase* e = eng->impl.get();
+    if (!e->phase_valid) throw HrtError(HRT_ERR_INVALID, "no fused call recorded yet");
+    CUDA_OK(cudaEventSynchronize(e->phase_ev[3]));
+    for (int i = 0; i < 3; ++i) CUDA_OK(cudaEventElapsedTime(&ms3[i], e->phase_ev[i], e->phase_ev[i + 1]));
+  });
 }
 
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable) {

@@ -132,6 +132,12 @@ __device__ __forceinline__ void load8(const bf16* p, float* o) {
   }
 }
 
+__device__ __forceinline__ void loadvec(const float* p, float* o) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+}
+__device__ __forceinline__ void loadvec(const bf16* p, float* o) { load8(p, o); }
+
 // ---------------------------------------------------------------------------
 // Ragged ("varlen") multi-head attention for whole sequences:
 //   encoder self-attention            infer.py:196-203   (full)
@@ -572,23 +578,31 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   sum = warp_sum(sum);
   __syncwarp();
   const float inv = 1.0f / sum;
-  float acc[DPL];
+  // PV: G groups of LPG lanes; group g takes keys j = g, g+G, ...; a lane owns
+  // VEC consecutive head dims and loads them as one 16-byte vector per key.
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int LPG = DH / VEC >= 1 ? DH / VEC : 1;
+  constexpr int G = 32 / LPG;
+  const int grp = lane / LPG, li = lane % LPG;
+  float acc[VEC];
 #pragma unroll
-  for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
 #pragma unroll 4
-  for (int j = 0; j < L; ++j) {
-    const T* vr = vrow(j);
+  for (int j = grp; j < L; j += G) {
     const float p = sc[j];
+    float vv[VEC];
+    loadvec(vrow(j) + li * VEC, vv);
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) {
-      const int c = lane + 32 * e;
-      if (c < DH) acc[e] = fmaf(p, to_f(vr[c]), acc[e]);
-    }
+    for (int e = 0; e < VEC; ++e) acc[e] = fmaf(p, vv[e], acc[e]);
   }
 #pragma unroll
-  for (int e = 0; e < DPL; ++e) {
-    const int c = lane + 32 * e;
-    if (c < DH) out[(size_t)r * out_stride + hoff + c] = from_f<T>(acc[e] * inv);
+  for (int o = LPG; o < 32; o <<= 1)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (grp == 0) {
+    T* dst = out + (size_t)r * out_stride + hoff + li * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) dst[e] = from_f<T>(acc[e] * inv);
   }
 }
 

@@ -43,8 +43,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // Epilogue protocols:
-//  element-wise (Epi::kRowWise == false): apply4(row, col, float4 v) for 4
-//    consecutive valid columns (N % 4 == 0 is required).
+//  element-wise (Epi::kRowWise == false): apply8(row0, col, float4 v[8], M)
+//    for rows row0 + 4 i (i < 8, rows >= M skipped), 4 consecutive columns
+//    (N % 4 == 0 is required).
 //  row-wise (Epi::kRowWise == true): State; begin(st,row,n0);
 //    chunk(st,row,col0,const float* v,int n); end(st,row,n0) per thread-row.
 template <int BN, int STAGES, class Epi>
@@ -180,15 +181,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
           __syncwarp();
           const int col = n0 + c + (lane & 7) * 4;
+          float4 vals[8];
 #pragma unroll
-          for (int r4 = 0; r4 < 32; r4 += 4) {
-            const int r = r4 + (lane >> 3);
-            const int row = rbase + r;
-            if (row < M && col < N) {
-              const float* s = stg + r * 33 + (lane & 7) * 4;
-              epi.apply4(row, col, make_float4(s[0], s[1], s[2], s[3]));
-            }
+          for (int i = 0; i < 8; ++i) {
+            const float* s = stg + (i * 4 + (lane >> 3)) * 33 + (lane & 7) * 4;
+            vals[i] = make_float4(s[0], s[1], s[2], s[3]);
           }
+          // rows rbase + (lane >> 3) + 4 i; all global loads of the group are
+          // issued before any store (memory-level parallelism)
+          if (col < N) epi.apply8(rbase + (lane >> 3), col, vals, M);
           __syncwarp();
         }
       }

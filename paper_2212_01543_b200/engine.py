@@ -123,6 +123,12 @@ class Engine:
         """Engine option, e.g. set_option("graphs", 0) to launch Stage I step by step."""
         self._check(self.lib.hrt_set_option(self._h, name.encode(), int(value)))
 
+    def phase_times(self):
+        """Device ms of the last fused call: encoder, Stage I, Stage II."""
+        ms = np.zeros(3, np.float32)
+        self._check(self.lib.hrt_phase_times(self._h, _ptr(ms, C.c_float)))
+        return dict(encoder=float(ms[0]), stage1=float(ms[1]), stage2=float(ms[2]))
+
     def timing_enable(self, kernel_class="all", enable=True):
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 

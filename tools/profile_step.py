@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--no-graph", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -32,6 +33,8 @@ def main():
     eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]),
                      dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", max_sentences=a.batch,
                      max_beam=spec["beam"])
+    if a.no_graph:
+        eng.set_option("graphs", 0)
     ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
     lens = [len(s) for s in srcs]
     for _ in range(2):

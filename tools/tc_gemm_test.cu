@@ -16,8 +16,9 @@ struct StoreEpi {
   static constexpr bool kRowWise = false;
   float* C;
   int ldc;
-  __device__ void apply4(int row, int col, float4 v) const {
-    *reinterpret_cast<float4*>(C + (size_t)row * ldc + col) = v;
+  __device__ void apply8(int row0, int col, const float4* v, int M) const {
+    for (int i = 0; i < 8; ++i)
+      if (row0 + 4 * i < M) *reinterpret_cast<float4*>(C + (size_t)(row0 + 4 * i) * ldc + col) = v[i];
   }
 };
 
