@@ -133,6 +133,8 @@ hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t 
 /* Device milliseconds of the last hrt_translate_batch's phases:
  * ms3[0] encoder (+cross-K/V), ms3[1] Stage I loop, ms3[2] Stage II + selection. */
 hrt_status hrt_phase_times(hrt_engine* eng, float* ms3);
+/* JSON {"call-site tag": [device ms, launches], ...} of the timed launches since enable. */
+hrt_status hrt_timing_report(hrt_engine* eng, char* buf, int64_t cap);
 /* Total device milliseconds and launch count of the timed class since enable. */
 hrt_status hrt_timing_read(hrt_engine* eng, double* total_ms, int64_t* launches, double* alg_bytes,
                            double* alg_flops);

@@ -14,6 +14,7 @@ template <typename T, class Epi>
 __global__ void __launch_bounds__(SG_THREADS) simt_gemm_kernel(const T* __restrict__ A, int lda,
                                                                const T* __restrict__ B, int ldb, int M, int N,
                                                                int K, const int* __restrict__ M_dev, Epi epi, int aligned4) {
+  pdl_enter();
   if (M_dev) M = *M_dev;
   const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
   if (m0 >= M) return;

@@ -83,7 +83,9 @@ struct EngineBase {
   // kernel-class timing
   int timed_class = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<const char*> ev_tag;
   size_t ev_used = 0;
+  const char* cur_tag = "untagged";  // call-site tag for the next launches
   double t_bytes = 0, t_flops = 0;
   int64_t t_launches = 0;
 
@@ -117,6 +119,8 @@ struct EngineBase {
           cudaEventCreate(&b);
           e->ev_pool.emplace_back(a, b);
         }
+        if (e->ev_tag.size() < e->ev_pool.size()) e->ev_tag.resize(e->ev_pool.size());
+        e->ev_tag[e->ev_used] = e->cur_tag;
         ev = &e->ev_pool[e->ev_used++];
         cudaEventRecord(ev->first, e->stream);
         e->t_bytes += bytes;
@@ -128,6 +132,28 @@ struct EngineBase {
       if (ev) cudaEventRecord(ev->second, e->stream);
       e->stats.kernel_launches += 1;
     }
+  };
+  bool pdl = true;  // programmatic dependent launch on every kernel
+  template <typename... KArgs, typename... Args>
+  void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t er = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (er != cudaSuccess) throw HrtError(HRT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(er));
+  }
+  struct Tag {
+    EngineBase* e;
+    const char* prev;
+    Tag(EngineBase* eng, const char* t) : e(eng), prev(eng->cur_tag) { e->cur_tag = t; }
+    ~Tag() { e->cur_tag = prev; }
   };
   void check_launch() {
     cudaError_t er = cudaGetLastError();
@@ -177,6 +203,10 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
+  // debug: drop kernel groups from the Stage-I step (timing attribution only;
+  // results are meaningless when nonzero). 1 LN, 2 attention, 4 GEMMs,
+  // 8 vocab, 16 select, 32 embed.
+  int s1_skip = 0;
   // outputs (device I/O staging)
   int *o_tokens, *o_lens, *o_calls;
   double* o_scores;
@@ -451,7 +481,10 @@ struct Engine : EngineBase {
     return mx;
   }
 
-  int nt_for_rows(int rows) const { return BF16 ? cdiv(V, choose_bn(rows, V)) : cdiv(V, 256); }
+  // vocab GEMM tile width: 256 whenever the vocabulary is large (fewer
+  // partials per row for the selection merge, one tile per CTA at small R)
+  int vocab_bn(int rows) const { return V >= 4096 ? 256 : choose_bn(rows, V); }
+  int nt_for_rows(int rows) const { return BF16 ? cdiv(V, vocab_bn(rows)) : cdiv(V, 256); }
 
   void carve(int phase, Plan& p, char* base) {
     if (phase == 0) {
@@ -581,7 +614,7 @@ struct Engine : EngineBase {
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN);
       const int tiles = cdiv(N, BN) * cdiv(M, TC_BM);  // M: count, or upper bound with M_dev
-      kern<<<std::min(tiles, num_sms), TC_THREADS, smem, stream>>>(ta, tb, M, N, K, M_dev, epi);
+      launch(kern, std::min(tiles, num_sms), TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi);
     }
   }
 
@@ -607,7 +640,7 @@ struct Engine : EngineBase {
         tc_launch<256, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
     } else {
       dim3 grid(cdiv(N, SG_BN), cdiv(M, SG_BM));
-      simt_gemm_kernel<T, Epi><<<grid, SG_THREADS, 0, stream>>>(A, lda, W, K, M, N, K, M_dev, epi,
+      launch(simt_gemm_kernel<T, Epi>, grid, SG_THREADS, 0, A, lda, W, K, M, N, K, M_dev, epi,
                                                                  epi.ld() % 4 == 0);
     }
     check_launch();
@@ -616,7 +649,7 @@ struct Engine : EngineBase {
   template <int NPL>
   void ln_launch(const float* x, const int* M_dev, int M, const float* g, const float* b, T* y, const int* out_row,
                  float* y32) {
-    layernorm_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(x, M_dev, M, d, g, b, y, out_row, y32);
+    launch(layernorm_kernel<T, NPL>, cdiv(M, 8), 256, 0, x, M_dev, M, d, g, b, y, out_row, y32);
   }
   void layernorm(const float* x, int M, const float* g, const float* b, T* y, const int* out_row = nullptr,
                  float* y32 = nullptr, const int* M_dev = nullptr) {
@@ -637,7 +670,7 @@ struct Engine : EngineBase {
   template <int NPL>
   void emb_launch(const int* ids, const int* pos, int pc, const int* pos_dev, const int* M_dev, int M, const float* g,
                   const float* b, float* x, T* y) {
-    embed_ln_kernel<T, NPL><<<cdiv(M, 8), 256, 0, stream>>>(ids, pos, pc, pos_dev, M_dev, M, d, emb_scale, E, pe, g, b,
+    launch(embed_ln_kernel<T, NPL>, cdiv(M, 8), 256, 0, ids, pos, pc, pos_dev, M_dev, M, d, emb_scale, E, pe, g, b,
                                                             x, y);
   }
   // M is the row count, or its upper bound when M_dev supplies it on device
@@ -662,7 +695,7 @@ struct Engine : EngineBase {
   void prefill_launch(dim3 grid, const int2* items, const T* q, int qs, const T* k, const T* v, int kvs, T* out,
                       int os, const int* q_off, const int* q_slot, const int* q_len, const int* kv_map,
                       const int* kv_off, const int* kv_len, const unsigned char* key_ok, int causal) {
-    attn_prefill_kernel<T, DH><<<grid, AP_WARPS * 32, 0, stream>>>(items, q, qs, k, v, kvs, out, os, q_off, q_slot,
+    launch(attn_prefill_kernel<T, DH>, grid, AP_WARPS * 32, 0, items, q, qs, k, v, kvs, out, os, q_off, q_slot,
                                                                    q_len, kv_map, kv_off, kv_len, key_ok, causal,
                                                                    att_scale);
   }
@@ -686,7 +719,7 @@ struct Engine : EngineBase {
 #define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
     if constexpr (BF16) {
       if (dh == 64) {
-        attn_prefill_mma_kernel<<<grid, AM_WARPS * 32, 0, stream>>>(it2, q, qs, k, v, kvs, out, os, q_off, q_slot,
+        launch(attn_prefill_mma_kernel, grid, AM_WARPS * 32, 0, it2, q, qs, k, v, kvs, out, os, q_off, q_slot,
                                                                    q_len, kv_map, kv_off, kv_len, key_ok, causal,
                                                                    att_scale);
         check_launch();
@@ -708,7 +741,7 @@ struct Engine : EngineBase {
   void decode_launch(int blocks, size_t smem, const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc,
                      const int* hist, int cap, int t, const int* t_dev, const int* row_seq, const int* kv_off,
                      const int* kv_len, const int* R_dev, int R, int lk_max, T* out) {
-    attn_decode_kernel<T, DH, SELF><<<blocks, 128, smem, stream>>>(q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, t_dev,
+    launch(attn_decode_kernel<T, DH, SELF>, blocks, 128, smem, q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, t_dev,
                                                                   row_seq, kv_off, kv_len, R_dev, R, H, lk_max,
                                                                   att_scale, out, d);
   }
@@ -739,7 +772,7 @@ struct Engine : EngineBase {
                    const int* M_dev = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
-      const int bn = choose_bn(R, V);
+      const int bn = vocab_bn(R);
       parts.ntiles = cdiv(V, bn);
       Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
       if (kt == 1) {
@@ -761,7 +794,7 @@ struct Engine : EngineBase {
                    2.0 * rn * (double)V * d);
           EpiStoreF32 epi{logits_buf, V};
           dim3 grid(cdiv(V, SG_BN), cdiv(rn, SG_BM));
-          simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y + (size_t)r0 * d, d, E, d, rn, V, d,
+          launch(simt_gemm_kernel<T, EpiStoreF32>, grid, SG_THREADS, 0, y + (size_t)r0 * d, d, E, d, rn, V, d,
                                                                             nullptr, epi, V % 4 == 0);
           check_launch();
         }
@@ -774,10 +807,10 @@ struct Engine : EngineBase {
         Scope sc(this, K_OTHER, 4.0 * rn * V, 0);
         dim3 grid(rn, parts.ntiles);
         if (kt == 1)
-          rowstats_from_logits_kernel<1><<<grid, 32, 0, stream>>>(logits_buf, V, V, nullptr, sub, 256, norm_allowed);
+          launch(rowstats_from_logits_kernel<1>, grid, 32, 0, logits_buf, V, V, nullptr, sub, 256, norm_allowed);
         else
-          rowstats_from_logits_kernel<KTOP_MAX>
-              <<<grid, 32, 0, stream>>>(logits_buf, V, V, nullptr, sub, 256, norm_allowed);
+          launch(rowstats_from_logits_kernel<KTOP_MAX>, grid, 32, 0, logits_buf, V, V, nullptr, sub, 256,
+                 norm_allowed);
         check_launch();
       }
     }
@@ -800,7 +833,7 @@ struct Engine : EngineBase {
       launch_vocab(y, y_cap, R, epi, choose_bn(R, V));
     } else {
       dim3 grid(cdiv(V, SG_BN), cdiv(R, SG_BM));
-      simt_gemm_kernel<T, EpiStoreF32><<<grid, SG_THREADS, 0, stream>>>(y, d, E, d, R, V, d, nullptr, epi, V % 4 == 0);
+      launch(simt_gemm_kernel<T, EpiStoreF32>, grid, SG_THREADS, 0, y, d, E, d, R, V, d, nullptr, epi, V % 4 == 0);
     }
     check_launch();
   }
@@ -811,6 +844,7 @@ struct Engine : EngineBase {
   // d_ids / d_pos hold the packed tokens; seq metadata in device arrays.
   // -------------------------------------------------------------------------
   void run_encoder(int M, int nseq, int max_len_seq, const int* off, const int* len, const int* items, int n_items) {
+    Tag _tg(this, "encoder");
     if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed max_src_tokens");
     if (Le > 0)
       embed_ln(d_ids, d_pos, 0, M, enc[0].ln1g, enc[0].ln1b, eb.x, eb.y);
@@ -841,28 +875,42 @@ struct Engine : EngineBase {
   // ctl != nullptr: graph mode -- R is the upper bound (grid sizing) and the
   // live row count, step and position are read from the device control block.
   void decoder_step(int R, int t, int pos, int cap, const int* feed, const int* hist, const int* row_seq,
-                    const int* kv_off, const int* kv_len, int max_src, StepCtl* ctl = nullptr) {
+                    const int* kv_off, const int* kv_len, int max_src, StepCtl* ctl = nullptr,
+                    bool do_embed = true) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     const int* td = ctl ? &ctl->t : nullptr;
-    embed_ln(feed, nullptr, pos, R, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, ctl ? &ctl->pos : nullptr, Rd);
+    Tag _tg4(this, "s1.embed_ln");
+    if (do_embed && !(s1_skip & 32)) embed_ln(feed, nullptr, pos, R, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, ctl ? &ctl->pos : nullptr, Rd);
     for (int i = 0; i < Ld; ++i) {
       const DecW& w = dec[i];
       T* kc = s1.kc + (size_t)i * R_max * cap_max * d;
       T* vc = s1.vc + (size_t)i * R_max * cap_max * d;
-      gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv}, Rd);
-      attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
+      Tag _tg10(this, "s1.qkv");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv}, Rd);
+      Tag _tg12(this, "s1.attn_self");
+      if (!(s1_skip & 2)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
                         nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd);
-      gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
-      layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y, nullptr, nullptr, Rd);
-      gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
-      attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
+      Tag _tg15(this, "s1.wo");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
+      Tag _tg17(this, "s1.ln2");
+      if (!(s1_skip & 1)) layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y, nullptr, nullptr, Rd);
+      Tag _tg19(this, "s1.qc");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
+      Tag _tg21(this, "s1.attn_cross");
+      if (!(s1_skip & 2)) attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
                          nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
                          2.0 * sizeof(T) * (double)R * max_src * d, nullptr, Rd);
-      gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
-      layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y, nullptr, nullptr, Rd);
-      gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
-      gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
-      if (i + 1 < Ld)
+      Tag _tg25(this, "s1.woc");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
+      Tag _tg27(this, "s1.ln3");
+      if (!(s1_skip & 1)) layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y, nullptr, nullptr, Rd);
+      Tag _tg29(this, "s1.w1");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
+      Tag _tg31(this, "s1.w2");
+      if (!(s1_skip & 4)) gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
+      Tag _tg34(this, "s1.ln_out");
+      if (s1_skip & 1) {
+      } else if (i + 1 < Ld)
         layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y, nullptr, nullptr, Rd);
       else
         layernorm(s1.x, R, dec_lng, dec_lnb, s1.y, nullptr, nullptr, Rd);
@@ -877,6 +925,7 @@ struct Engine : EngineBase {
   void decoder_parallel(int M2, int nc, int max_slot, int max_src, const int* off, const int* slot,
                         const int* qlen, const int* kv_map, const int* src_off, const int* src_len,
                         const unsigned char* key_ok, int causal, const int* out_row, const int* items, int n_items) {
+    Tag _tg(this, "stage2.decoder");
     embed_ln(s2.ids, s2.pos, 0, M2, dec[0].ln1g, dec[0].ln1b, s2.x, s2.y);
     for (int i = 0; i < Ld; ++i) {
       const DecW& w = dec[i];
@@ -995,7 +1044,7 @@ struct Engine : EngineBase {
         p_rowseq_h[r] = row_seq[r];
       }
     CUDA_OK(cudaMemcpyAsync(s_rowseq, p_rowseq_h.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream));
-    stage1_init_kernel<<<cdiv(rows, 128), 128, 0, stream>>>(rows, cap, BOS_ID, s_feed, s_done, s_nsteps, s_forced,
+    launch(stage1_init_kernel, cdiv(rows, 128), 128, 0, rows, cap, BOS_ID, s_feed, s_done, s_nsteps, s_forced,
                                                            s_score, s_hist);
     check_launch();
     stats.kernel_launches++;
@@ -1021,7 +1070,7 @@ struct Engine : EngineBase {
       for (int r0 = 0; r0 < p_rows; r0 += logit_rows) {
         const int rn = std::min(logit_rows, p_rows - r0);
         full_logits(s1.y + (size_t)r0 * d, R_max - r0, rn, s1.logits);
-        logsoftmax_rows_kernel<<<rn, 256, 0, stream>>>(s1.logits, V, V);
+        launch(logsoftmax_rows_kernel, rn, 256, 0, s1.logits, V, V);
         check_launch();
         stats.kernel_launches++;
         CUDA_OK(cudaMemcpyAsync(logp_out + (size_t)r0 * V, s1.logits, (size_t)rn * V * sizeof(float),
@@ -1043,7 +1092,7 @@ struct Engine : EngineBase {
     }
     if (ident) return;
     CUDA_OK(cudaMemcpyAsync(s_parents, parents, p_rows * sizeof(int), cudaMemcpyHostToDevice, stream));
-    reorder_hist_kernel<<<p_rows, 128, 0, stream>>>(s_parents, s_hist, s_hist2, p_rows, p_cap, p_len);
+    launch(reorder_hist_kernel, p_rows, 128, 0, s_parents, s_hist, s_hist2, p_rows, p_cap, p_len);
     check_launch();
     stats.kernel_launches++;
     std::swap(s_hist, s_hist2);
@@ -1125,11 +1174,13 @@ struct Engine : EngineBase {
     const int64_t before = stats.kernel_launches;
     CUDA_OK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     try {
-      decoder_step(bucket, 0, 0, cap_max, s_feed, s_hist, nullptr, s_srcoff, s_srclen, Lmax, s_ctl);
-      vocab_parts(s1.y, R_max, bucket, s1.parts, 1, 0, s1.logits, &s_ctl->R);
-      greedy_select_kernel<1><<<cdiv(bucket, 4), 128, 0, stream>>>(s1.parts, gs, bucket, 0, s_ctl);
-      check_launch();
-      stage1_advance_kernel<<<1, 1, 0, stream>>>(s_ctl, s_alive, h);
+      decoder_step(bucket, 0, 0, cap_max, s_feed, s_hist, nullptr, s_srcoff, s_srclen, Lmax, s_ctl, false);
+      if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, bucket, s1.parts, 1, 0, s1.logits, &s_ctl->R);
+      if (!(s1_skip & 16)) {
+        launch(greedy_select_kernel<T, 1>, cdiv(bucket, 4), 128, 0, s1.parts, gs, bucket, 0, 0, s_ctl);
+        check_launch();
+      }
+      launch(stage1_advance_kernel, 1, 1, 0, s_ctl, s_alive, h);
       check_launch();
     } catch (...) {
       cudaGraph_t dummy;
@@ -1148,6 +1199,14 @@ struct Engine : EngineBase {
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
+    else if (name == "stage1_skip") {
+      s1_skip = value;
+      for (auto& kv : loop_graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      }
+      loop_graphs.clear();
+    }
     else
       throw HrtError(HRT_ERR_INVALID, "unknown option " + name);
   }
@@ -1161,6 +1220,7 @@ struct Engine : EngineBase {
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void transpose_convert_kernel(const float* __restrict__ s, int K, int N, T* __restrict__ dst) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -1176,6 +1236,7 @@ __global__ void transpose_convert_kernel(const float* __restrict__ s, int K, int
 
 template <typename T>
 __global__ void convert_kernel(const float* __restrict__ s, size_t n, T* __restrict__ dst) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     dst[i] = from_f<T>(s[i]);
 }
@@ -1183,18 +1244,19 @@ __global__ void convert_kernel(const float* __restrict__ s, size_t n, T* __restr
 template <typename T>
 void Engine<T>::transpose_convert(const float* s, int K, int N, T* dst) {
   dim3 grid(cdiv(N, 32), cdiv(K, 32));
-  transpose_convert_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(s, K, N, dst);
+  launch(transpose_convert_kernel<T>, grid, dim3(32, 8), 0, s, K, N, dst);
   check_launch();
 }
 template <typename T>
 void Engine<T>::convert(const float* s, size_t n, T* dst) {
-  convert_kernel<T><<<1024, 256, 0, stream>>>(s, n, dst);
+  launch(convert_kernel<T>, 1024, 256, 0, s, n, dst);
   check_launch();
 }
 
 // argmax / renormalised log-prob over non-excluded ids (infer.py:401-418)
 __global__ void argmax_lp_kernel(const float* __restrict__ logits, int V, const unsigned char* __restrict__ excl,
                                  int* __restrict__ amax, float* __restrict__ lp) {
+  pdl_enter();
   const int row = blockIdx.x;
   const float* l = logits + (size_t)row * V;
   __shared__ float sv[32];
@@ -1268,7 +1330,7 @@ void Engine<T>::argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, 
   int* d_amax = meta_put(cur, std::vector<int>(M2, 0));
   float* d_lp = reinterpret_cast<float*>(meta_put(cur, std::vector<int>(M2, 0)));
   meta_flush(cur);
-  argmax_lp_kernel<<<M2, 256, 0, stream>>>(p_logits, V, d_ex, d_amax, d_lp);
+  launch(argmax_lp_kernel, M2, 256, 0, p_logits, V, d_ex, d_amax, d_lp);
   check_launch();
   stats.kernel_launches++;
   CUDA_OK(cudaMemcpyAsync(amax, d_amax, M2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -1370,7 +1432,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   {
     Scope sc(this, K_OTHER, 8.0 * Mtok, 0);
-    gather_sentences_kernel<<<B, 128, 0, stream>>>(src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B);
+    launch(gather_sentences_kernel, B, 128, 0, src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B);
     check_launch();
   }
   // ---- phase 1: encoder ----
@@ -1383,12 +1445,17 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   const int capA = cap_max;
   {
     Scope sc(this, K_OTHER, 0, 0);
-    stage1_init_kernel<<<cdiv(B, 128), 128, 0, stream>>>(B, capA, 4 + (k - 2) /*BOS_k*/, s_feed, s_done, s_nsteps,
+    launch(stage1_init_kernel, cdiv(B, 128), 128, 0, B, capA, 4 + (k - 2) /*BOS_k*/, s_feed, s_done, s_nsteps,
                                                         s_forced, s_score, s_hist);
     check_launch();
   }
   CUDA_OK(cudaMemcpyAsync(s_caps, d_caps, B * sizeof(int), cudaMemcpyDeviceToDevice, stream));
-  GreedyState gs{s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
+  GreedyState gs{E, pe, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, emb_scale, d,
+                 s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
+  {  // step-0 input (BOS_k at position 0); later steps are embedded by the selection kernel
+    Tag _tg(this, "s1.embed_ln");
+    embed_ln(s_feed, nullptr, 0, alive.empty() ? 0 : alive[0], dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
+  }
   if (BF16 && use_graphs && timed_class == 0) {
     // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
     int bucket = 1;
@@ -1401,10 +1468,14 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     for (int t = 0; t < max_cap; ++t) {
       const int R = alive[t];
       if (R == 0) break;
-      decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src);
-      vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
+      decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src, nullptr, false);
+      {
+        Tag _tg(this, "s1.vocab");
+        vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
+      }
+      Tag _tg(this, "s1.select");
       Scope sc(this, K_OTHER, 0, 0);
-      greedy_select_kernel<1><<<cdiv(R, 4), 128, 0, stream>>>(s1.parts, gs, R, t, nullptr);
+      launch(greedy_select_kernel<T, 1>, cdiv(R, 4), 128, 0, s1.parts, gs, R, t, k, nullptr);
       check_launch();
     }
   }
@@ -1412,16 +1483,17 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   // ---- phase 3: Stage II over the greedy chain (b_nat = 1) ----
   {
     Scope sc(this, K_OTHER, 0, 0);
-    stage2_build_kernel<<<B, 128, 0, stream>>>(s_anchors, capA, d_seqmap, s_nsteps, d_off2, d_slot, B, k, s2.ids,
+    launch(stage2_build_kernel, B, 128, 0, s_anchors, capA, d_seqmap, s_nsteps, d_off2, d_slot, B, k, s2.ids,
                                                s2.pos, d_qlen2);
     check_launch();
   }
   decoder_parallel(M2, B, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
                    d_s2_items, (int)s2_items.size() / 2);
+  Tag _tg2(this, "stage2.vocab");
   vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
   {
     Scope sc(this, K_OTHER, 0, 0);
-    rowstat_kernel<1><<<cdiv(Mm, 4), 128, 0, stream>>>(s2.parts, Mm, 1, s2.mstat);
+    launch(rowstat_kernel<1>, cdiv(Mm, 4), 128, 0, s2.parts, Mm, 1, s2.mstat);
     check_launch();
   }
   Stage2Out so;
@@ -1433,7 +1505,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   so.out_index = d_perm;
   {
     Scope sc(this, K_OTHER, 0, 0);
-    stage2_finish_kernel<<<cdiv(B, 4), 128, 0, stream>>>(s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, d_seqmap,
+    launch(stage2_finish_kernel, cdiv(B, 4), 128, 0, s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, d_seqmap,
                                                         s_score, s_nsteps, s_forced, k, alpha, Lmax, B, so);
     check_launch();
   }
@@ -1584,6 +1656,29 @@ hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t 
     e->ev_used = 0;
     e->t_bytes = e->t_flops = 0;
     e->t_launches = 0;
+  });
+}
+
+hrt_status hrt_timing_report(hrt_engine* eng, char* buf, int64_t cap) {
+  return guarded(eng, [&] {
+    EngineBase* e = eng->impl.get();
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    std::map<std::string, std::pair<double, int>> agg;
+    for (size_t i = 0; i < e->ev_used; ++i) {
+      float m = 0;
+      CUDA_OK(cudaEventElapsedTime(&m, e->ev_pool[i].first, e->ev_pool[i].second));
+      auto& a = agg[e->ev_tag[i] ? e->ev_tag[i] : "untagged"];
+      a.first += m;
+      a.second += 1;
+    }
+    std::string s = "{";
+    for (auto& kv : agg) {
+      if (s.size() > 1) s += ", ";
+      s += "\"" + kv.first + "\": [" + std::to_string(kv.second.first) + ", " + std::to_string(kv.second.second) + "]";
+    }
+    s += "}";
+    if ((int64_t)s.size() + 1 > cap) throw HrtError(HRT_ERR_INVALID, "report buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
   });
 }
 

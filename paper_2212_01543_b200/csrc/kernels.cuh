@@ -22,6 +22,7 @@ __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restri
                                 const int* __restrict__ pos_dev, const int* __restrict__ M_dev, int M, int d, float scale, const T* __restrict__ E,
                                 const float* __restrict__ pe, const float* __restrict__ g,
                                 const float* __restrict__ b, float* __restrict__ x, T* __restrict__ y) {
+  pdl_enter();
   if (M_dev) M = *M_dev;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -70,6 +71,7 @@ template <typename T, int NPL>
 __global__ void layernorm_kernel(const float* __restrict__ x, const int* __restrict__ M_dev, int M, int d,
                                  const float* __restrict__ g, const float* __restrict__ b, T* __restrict__ y,
                                  const int* __restrict__ out_row, float* __restrict__ y32) {
+  pdl_enter();
   if (M_dev) M = *M_dev;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(AP_WARPS * 32) attn_prefill_kernel(
     const int* __restrict__ q_slot, const int* __restrict__ q_len, const int* __restrict__ kv_map,
     const int* __restrict__ kv_off, const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok,
     int causal, float scale) {
+  pdl_enter();
   __shared__ __align__(16) float Ks[AP_KC][DH];
   __shared__ __align__(16) float Vs[AP_KC][DH];
   __shared__ float kbias[AP_KC];
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(AM_WARPS * 32) attn_prefill_mma_kernel(
     const int* __restrict__ q_slot, const int* __restrict__ q_len, const int* __restrict__ kv_map,
     const int* __restrict__ kv_off, const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok,
     int causal, float scale) {
+  pdl_enter();
   constexpr int DH = 64;
   __shared__ __align__(16) bf16 Qs[32][AM_LD];
   __shared__ __align__(16) bf16 Ks[AM_KC][AM_LD];
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const int* __restrict__ t_dev, const int* __restrict__ row_seq, const int* __restrict__ kv_off,
     const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale,
     T* __restrict__ out, int out_stride) {
+  pdl_enter();
   extern __shared__ float sm[];
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;
   if (R_dev) R = *R_dev;
@@ -761,6 +766,7 @@ template <int KT>
 __global__ void rowstats_from_logits_kernel(const float* __restrict__ logits, int ld, int V,
                                             const int* __restrict__ row_map, VocabParts parts, int tile_w,
                                             int norm_allowed) {
+  pdl_enter();
   const int row = blockIdx.x, tile = blockIdx.y, lane = threadIdx.x;
   const int src = row_map ? row_map[row] : row;
   const float* l = logits + (size_t)src * ld;
@@ -887,6 +893,16 @@ struct StepCtl {
 };
 
 struct GreedyState {
+  // next-step embedding (x = E[tok] * sqrt(d) + PE[(t+1) k], y = LN1(x)),
+  // fused into the selection so Stage I needs no separate embed kernel
+  const void* E;
+  const float* pe;
+  const float* ln_g;
+  const float* ln_b;
+  float* x;
+  void* y;
+  float scale;
+  int d;
   int* feed;       // [rows] next fed token
   int* done;       // [rows]
   int* nsteps;     // [rows] steps taken when finished
@@ -897,37 +913,94 @@ struct GreedyState {
   int cap;
 };
 
-template <int KT>
-__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, StepCtl* ctl) {
+// Embedding + LayerNorm of one row by one warp (generic d <= 1024).
+template <typename T>
+__device__ __forceinline__ void warp_embed_ln(const T* __restrict__ E, const float* __restrict__ pe,
+                                              const float* __restrict__ g, const float* __restrict__ b, float scale,
+                                              int d, int tok, int pos, float* __restrict__ x, T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  float v[32];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = 0.f;
+    if (j < d) {
+      v[i] = __fadd_rn(__fmul_rn(to_f(E[(size_t)tok * d + j]), scale), pe[(size_t)pos * d + j]);
+      s += v[i];
+    }
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int j = lane + 32 * i;
+    if (j < d) {
+      const float c = v[i] - mean;
+      q += c * c;
+    }
+  }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / d + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int j = lane + 32 * i;
+    if (j < d) {
+      x[j] = v[i];
+      y[j] = from_f<T>((v[i] - mean) * inv * g[j] + b[j]);
+    }
+  }
+}
+
+template <typename T, int KT>
+__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, int k, StepCtl* ctl) {
+  pdl_enter();
   if (ctl) {
     R = ctl->R;
     t = ctl->t;
+    k = ctl->k;
   }
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
-  if (st.done[row]) return;
-  const RowStat rs = merge_row<KT>(parts, row, 1);
-  if (lane != 0) return;
-  const bool last = (t == st.caps[row] - 1);
-  const int tok = last ? EOS_ID : rs.id[0];
-  const float logit = last ? rs.eos : rs.val[0];
-  const float lp = (logit - rs.mx) - rs.lse;
-  st.score[row] += (double)lp;
-  st.anchors[(size_t)row * st.cap + t] = tok;
-  st.feed[row] = tok;
-  if (tok == EOS_ID) {
-    st.done[row] = 1;
-    st.nsteps[row] = t + 1;
-    st.forced[row] = last ? 1 : 0;
-    if (ctl) atomicAdd(&ctl->finished, 1);
+  int tok;
+  if (st.done[row]) {
+    tok = st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
+  } else {
+    const RowStat rs = merge_row<KT>(parts, row, 1);
+    tok = 0;
+    if (lane == 0) {
+      const bool last = (t == st.caps[row] - 1);
+      int best = rs.id[0];
+      float bl = rs.val[0];
+      if (best == 0x7fffffff) {  // non-finite logits: finish the row rather than emit a bogus id
+        best = EOS_ID;
+        bl = rs.eos;
+      }
+      tok = last ? EOS_ID : best;
+      const float logit = last ? rs.eos : bl;
+      const float lp = (logit - rs.mx) - rs.lse;
+      st.score[row] += (double)lp;
+      st.anchors[(size_t)row * st.cap + t] = tok;
+      st.feed[row] = tok;
+      if (tok == EOS_ID) {
+        st.done[row] = 1;
+        st.nsteps[row] = t + 1;
+        st.forced[row] = last ? 1 : 0;
+        if (ctl) atomicAdd(&ctl->finished, 1);
+      }
+    }
+    tok = __shfl_sync(0xffffffffu, tok, 0);
   }
+  if (st.x != nullptr)
+    warp_embed_ln<T>(static_cast<const T*>(st.E), st.pe, st.ln_g, st.ln_b, st.scale, st.d, tok, (t + 1) * k,
+                     st.x + (size_t)row * st.d, static_cast<T*>(st.y) + (size_t)row * st.d);
 }
 
 // End of one graph-resident Stage-I step: advance the control block and
 // decide whether the WHILE node runs another step (decoding.py:102, :149).
 __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ alive,
                                       cudaGraphConditionalHandle handle) {
+  pdl_enter();
   const int t = ctl->t + 1;
   const bool more = t < ctl->max_cap && ctl->finished < ctl->nrows && alive[t] > 0;
   if (more) {
@@ -941,6 +1014,7 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.
 template <int KT>
 __global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restrict__ out) {
+  pdl_enter();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= R) return;
   const RowStat rs = merge_row<KT>(parts, row, kt);
@@ -957,6 +1031,7 @@ __global__ void stage2_build_kernel(const int* __restrict__ anchors, int cap, co
                                     const int* __restrict__ cand_len, const int* __restrict__ off,
                                     const int* __restrict__ slot, int C, int k, int* __restrict__ ids,
                                     int* __restrict__ pos, int* __restrict__ qlen) {
+  pdl_enter();
   const int c = blockIdx.x;
   if (c >= C) return;
   const int m = cand_len[c];
@@ -996,6 +1071,7 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
                                      const int* __restrict__ cand_row, const double* __restrict__ s_at,
                                      const int* __restrict__ nsteps, const int* __restrict__ forced, int k,
                                      float alpha, int max_len, int S, Stage2Out out) {
+  pdl_enter();
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= S) return;
@@ -1035,6 +1111,7 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
     int tok = -1;
     if (j < T) {
       tok = ((j + 1) % k != 0) ? mstat[mo + j - (j + 1) / k].id[0] : ids[o + j];
+      if (tok == 0x7fffffff) tok = EOS_ID;
     }
     const unsigned ball = __ballot_sync(0xffffffffu, j < T && tok == EOS_ID);
     if (ball) {
@@ -1044,7 +1121,8 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
   }
   const int n = min(first_eos, max_len);
   for (int j = lane; j < n; j += 32) {
-    const int tok = ((j + 1) % k != 0) ? mstat[mo + j - (j + 1) / k].id[0] : ids[o + j];
+    int tok = ((j + 1) % k != 0) ? mstat[mo + j - (j + 1) / k].id[0] : ids[o + j];
+    if (tok == 0x7fffffff) tok = EOS_ID;
     out.tokens[(size_t)dst * max_len + j] = tok;
   }
   if (lane == 0) {
@@ -1065,6 +1143,7 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
 __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* __restrict__ src_off,
                                         const int* __restrict__ dst_off, const int* __restrict__ perm,
                                         int* __restrict__ dst, int* __restrict__ pos, int n) {
+  pdl_enter();
   const int i = blockIdx.x;
   if (i >= n) return;
   const int p = perm[i];
@@ -1078,6 +1157,7 @@ __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* 
 // Stage-I row initialisation: feed = bos, history slot map = identity.
 __global__ void stage1_init_kernel(int R, int cap, int bos, int* feed, int* done, int* nsteps, int* forced,
                                    double* score, int* hist) {
+  pdl_enter();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   feed[r] = bos;
@@ -1092,6 +1172,7 @@ __global__ void stage1_init_kernel(int R, int cap, int bos, int* feed, int* done
 // from old row parents[j]; history slots 0..t-1 follow the parent.
 __global__ void reorder_hist_kernel(const int* __restrict__ parents, const int* __restrict__ hist_in,
                                     int* __restrict__ hist_out, int R, int cap, int t) {
+  pdl_enter();
   const int r = blockIdx.x;
   if (r >= R) return;
   const int p = parents[r];
@@ -1101,6 +1182,7 @@ __global__ void reorder_hist_kernel(const int* __restrict__ parents, const int* 
 
 // Full-row log-softmax in place (protocol-face step(), infer.py:296-301).
 __global__ void logsoftmax_rows_kernel(float* __restrict__ l, int ld, int V) {
+  pdl_enter();
   const int row = blockIdx.x;
   float* x = l + (size_t)row * ld;
   __shared__ float red[32];
@@ -1134,6 +1216,7 @@ __global__ void logsoftmax_rows_kernel(float* __restrict__ l, int ld, int V) {
 
 // fp32 -> bf16 conversion (weights, once at engine creation)
 __global__ void f32_to_bf16_kernel(const float* __restrict__ a, bf16* __restrict__ b, size_t n) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     b[i] = __float2bfloat16_rn(a[i]);
 }

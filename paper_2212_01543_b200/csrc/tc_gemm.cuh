@@ -13,6 +13,7 @@
 //                 rows; row-wise epilogues (vocab softmax statistics) keep
 //                 one row per thread.
 #pragma once
+#include "common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace hrt {
@@ -61,17 +62,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  if (M_dev != nullptr) M = *M_dev;
-  const int m_tiles = (M + TC_BM - 1) / TC_BM;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  if ((int)blockIdx.x >= num_tiles) return;  // CTA-uniform, before any allocation
-
+  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_kb = K / TC_BK;
   constexpr uint32_t TMEM_COLS = tmem_cols_for<BN>();
 
+  // setup that does not depend on the previous kernel overlaps its tail (PDL)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -90,6 +87,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  if (M_dev != nullptr) M = *M_dev;
+  const int m_tiles = (M + TC_BM - 1) / TC_BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
 
   if (warp == 0) {
     if (lane == 0) {

@@ -132,6 +132,14 @@ class Engine:
     def timing_enable(self, kernel_class="all", enable=True):
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 
+    def timing_report(self):
+        """{call-site tag: (device ms, launches)} of the timed launches since timing_enable."""
+        import json
+
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.lib.hrt_timing_report(self._h, buf, len(buf)))
+        return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
+
     def timing_read(self):
         ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         self._check(self.lib.hrt_timing_read(self._h, C.byref(ms), C.byref(n), C.byref(b), C.byref(f)))
