@@ -193,6 +193,12 @@ struct Engine : EngineBase {
   // Stage-I state
   int *s_feed, *s_done, *s_nsteps, *s_forced, *s_anchors, *s_caps, *s_hist, *s_hist2, *s_rowseq, *s_parents;
   double* s_score;
+  // device beam search state (fused b_at > 1 path)
+  int *b_greedy, *b_anchors2, *b_live, *b_nfin, *b_gdone, *b_fcount, *b_fgslot, *b_flist, *b_flen, *b_fforced,
+      *b_ftok;
+  double* b_fscore;
+  int *c_off, *c_len, *c_forced;
+  double* c_sat;
   StepCtl* s_ctl;
   int *s_alive, *s_srcoff, *s_srclen;
   // captured Stage-I loops (conditional WHILE graph), keyed by row bucket
@@ -227,6 +233,7 @@ struct Engine : EngineBase {
     float* x;
     T *y, *qkv, *qc, *ctx, *hid, *kc, *vc;
     VocabParts parts;
+    RowStat* rowstat;
     float* logits;
   } s1;
   struct S2Bufs {
@@ -508,6 +515,7 @@ struct Engine : EngineBase {
       s1.parts.val = p.take<float>(base, ntot * KTOP_MAX);
       s1.parts.id = p.take<int>(base, ntot * KTOP_MAX);
       s1.parts.eos = p.take<float>(base, R_max);
+      s1.rowstat = p.take<RowStat>(base, R_max);
       s1.logits = p.take<float>(base, (size_t)std::min(R_max, logit_rows) * V);
     } else {
       s2.x = p.take<float>(base, (size_t)M2_max * d);
@@ -552,6 +560,22 @@ struct Engine : EngineBase {
       s_hist = p.take<int>(base, (size_t)R_max * cap_max);
       s_hist2 = p.take<int>(base, (size_t)R_max * cap_max);
       s_score = p.take<double>(base, R_max);
+      b_greedy = p.take<int>(base, R_max);
+      b_anchors2 = p.take<int>(base, (size_t)R_max * cap_max);
+      b_live = p.take<int>(base, Bmax);
+      b_nfin = p.take<int>(base, Bmax);
+      b_gdone = p.take<int>(base, Bmax);
+      b_fcount = p.take<int>(base, Bmax);
+      b_fgslot = p.take<int>(base, Bmax);
+      b_flist = p.take<int>(base, (size_t)Bmax * beam_max);
+      b_fscore = p.take<double>(base, (size_t)Bmax * (beam_max + 2));
+      b_flen = p.take<int>(base, (size_t)Bmax * (beam_max + 2));
+      b_fforced = p.take<int>(base, (size_t)Bmax * (beam_max + 2));
+      b_ftok = p.take<int>(base, (size_t)Bmax * (beam_max + 2) * cap_max);
+      c_off = p.take<int>(base, (size_t)Bmax * beam_max);
+      c_len = p.take<int>(base, (size_t)Bmax * beam_max);
+      c_sat = p.take<double>(base, (size_t)Bmax * beam_max);
+      c_forced = p.take<int>(base, (size_t)Bmax * beam_max);
       o_tokens = p.take<int>(base, (size_t)Bmax * Lmax);
       o_lens = p.take<int>(base, Bmax);
       o_calls = p.take<int>(base, Bmax);
@@ -739,23 +763,23 @@ struct Engine : EngineBase {
 
   template <int DH, bool SELF>
   void decode_launch(int blocks, size_t smem, const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc,
-                     const int* hist, int cap, int t, const int* t_dev, const int* row_seq, const int* kv_off,
-                     const int* kv_len, const int* R_dev, int R, int lk_max, T* out) {
-    launch(attn_decode_kernel<T, DH, SELF>, blocks, 128, smem, q, qs, kn, vn, ns, kc, vc, d, hist, cap, t, t_dev,
+                     const int* hist, const int* hist2, int cap, int t, const int* t_dev, const int* row_seq,
+                     const int* kv_off, const int* kv_len, const int* R_dev, int R, int lk_max, T* out) {
+    launch(attn_decode_kernel<T, DH, SELF>, blocks, 128, smem, q, qs, kn, vn, ns, kc, vc, d, hist, hist2, cap, t, t_dev,
                                                                   row_seq, kv_off, kv_len, R_dev, R, H, lk_max,
                                                                   att_scale, out, d);
   }
   template <bool SELF>
   void attn_decode(const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc, const int* hist, int cap, int t,
                    const int* row_seq, const int* kv_off, const int* kv_len, int R, int lk_max, T* out,
-                   double bytes, const int* t_dev = nullptr, const int* R_dev = nullptr) {
+                   double bytes, const int* t_dev = nullptr, const int* R_dev = nullptr, const int* hist2 = nullptr) {
     if (R <= 0) return;
     Scope sc(this, K_ATTN, bytes, 0.0);
     const int nwarp = 4;
     lk_max = std::max(lk_max, 1);
     const size_t smem = (size_t)nwarp * lk_max * sizeof(float);
     const int blocks = cdiv(R * H, nwarp);
-#define HRT_DC(DHV) decode_launch<DHV, SELF>(blocks, smem, q, qs, kn, vn, ns, kc, vc, hist, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, lk_max, out)
+#define HRT_DC(DHV) decode_launch<DHV, SELF>(blocks, smem, q, qs, kn, vn, ns, kc, vc, hist, hist2, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, lk_max, out)
     switch (dh) {
       case 8: HRT_DC(8); break;
       case 16: HRT_DC(16); break;
@@ -876,7 +900,7 @@ struct Engine : EngineBase {
   // live row count, step and position are read from the device control block.
   void decoder_step(int R, int t, int pos, int cap, const int* feed, const int* hist, const int* row_seq,
                     const int* kv_off, const int* kv_len, int max_src, StepCtl* ctl = nullptr,
-                    bool do_embed = true) {
+                    bool do_embed = true, const int* hist2 = nullptr) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     const int* td = ctl ? &ctl->t : nullptr;
     Tag _tg4(this, "s1.embed_ln");
@@ -889,7 +913,7 @@ struct Engine : EngineBase {
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv}, Rd);
       Tag _tg12(this, "s1.attn_self");
       if (!(s1_skip & 2)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
-                        nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd);
+                        nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd, hist2);
       Tag _tg15(this, "s1.wo");
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
       Tag _tg17(this, "s1.ln2");
@@ -1154,11 +1178,81 @@ struct Engine : EngineBase {
     stats.decoder_calls += 1;
   }
 
-  // Capture (once per row bucket) the Stage-I step -- decoder layers, vocab
-  // statistics, greedy selection, loop advance -- as the body of a
-  // conditional WHILE node. Every step-varying value lives in s_ctl.
-  LoopGraph& loop_graph(int bucket, const GreedyState& gs) {
-    LoopGraph& lg = loop_graphs[bucket];
+  BeamState beam_state(int beam, int bnat) {
+    BeamState bs;
+    bs.beam = beam;
+    bs.bnat = bnat;
+    bs.cap = cap_max;
+    bs.feed = s_feed;
+    bs.score = s_score;
+    bs.greedy = b_greedy;
+    bs.anchors[0] = s_anchors;
+    bs.anchors[1] = b_anchors2;
+    bs.hist[0] = s_hist;
+    bs.hist[1] = s_hist2;
+    bs.live_n = b_live;
+    bs.done = s_done;
+    bs.nsteps = s_nsteps;
+    bs.n_fin = b_nfin;
+    bs.greedy_done = b_gdone;
+    bs.caps = s_caps;
+    bs.f_count = b_fcount;
+    bs.f_list = b_flist;
+    bs.f_gslot = b_fgslot;
+    bs.f_score = b_fscore;
+    bs.f_len = b_flen;
+    bs.f_forced = b_fforced;
+    bs.f_tok = b_ftok;
+    bs.E = E;
+    bs.pe = pe;
+    bs.ln_g = dec[0].ln1g;
+    bs.ln_b = dec[0].ln1b;
+    bs.x = s1.x;
+    bs.y = s1.y;
+    bs.scale = emb_scale;
+    bs.d = d;
+    return bs;
+  }
+
+  // One Stage-I step for R live rows (R is an upper bound when ctl != null):
+  // decoder layers, vocab statistics, selection (greedy or beam), which also
+  // embeds the next step's inputs.
+  void stage1_step(int R, int t, int k, int beam, int max_src, const int* src_off, const int* src_len,
+                   const GreedyState& gs, const BeamState& bs, StepCtl* ctl) {
+    const int* Rd = ctl ? &ctl->R : nullptr;
+    if (beam == 1) {
+      decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false);
+      {
+        Tag _tg(this, "s1.vocab");
+        if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd);
+      }
+      Tag _tg(this, "s1.select");
+      Scope sc(this, K_OTHER, 0, 0);
+      if (!(s1_skip & 16)) {
+        launch(greedy_select_kernel<T, 1>, cdiv(R, 4), 128, 0, s1.parts, gs, R, t, k, ctl);
+        check_launch();
+      }
+    } else {
+      decoder_step(R, t, t * k, cap_max, s_feed, s_hist, s_rowseq, src_off, src_len, max_src, ctl, false, s_hist2);
+      {
+        Tag _tg(this, "s1.vocab");
+        vocab_parts(s1.y, R_max, R, s1.parts, KTOP_MAX, 0, s1.logits, Rd);
+      }
+      Tag _tg(this, "s1.select");
+      Scope sc(this, K_OTHER, 0, 0);
+      launch(rowstat_kernel<KTOP_MAX>, cdiv(R, 4), 128, 0, s1.parts, R, beam + 1, s1.rowstat, Rd);
+      check_launch();
+      const int S = cdiv(R, beam);
+      launch(beam_select_kernel<T>, cdiv(S, 4), 128, 0, s1.rowstat, bs, S, t, k, ctl);
+      check_launch();
+    }
+  }
+
+  // Capture (once per row bucket and beam width) the Stage-I step as the body
+  // of a conditional WHILE node. Every step-varying value lives in s_ctl.
+  LoopGraph& loop_graph(int bucket, int beam, const GreedyState& gs, const BeamState& bs) {
+    // captured kernel parameters depend on the bucket, beam and b_nat (finished-store layout)
+    LoopGraph& lg = loop_graphs[(bucket * 16 + beam) * 16 + bs.bnat];
     if (lg.exec) return lg;
     CUDA_OK(cudaGraphCreate(&lg.graph, 0));
     cudaGraphConditionalHandle h;
@@ -1174,12 +1268,7 @@ struct Engine : EngineBase {
     const int64_t before = stats.kernel_launches;
     CUDA_OK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     try {
-      decoder_step(bucket, 0, 0, cap_max, s_feed, s_hist, nullptr, s_srcoff, s_srclen, Lmax, s_ctl, false);
-      if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, bucket, s1.parts, 1, 0, s1.logits, &s_ctl->R);
-      if (!(s1_skip & 16)) {
-        launch(greedy_select_kernel<T, 1>, cdiv(bucket, 4), 128, 0, s1.parts, gs, bucket, 0, 0, s_ctl);
-        check_launch();
-      }
+      stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
       launch(stage1_advance_kernel, 1, 1, 0, s_ctl, s_alive, h);
       check_launch();
     } catch (...) {
@@ -1188,7 +1277,7 @@ struct Engine : EngineBase {
       throw;
     }
     CUDA_OK(cudaStreamEndCapture(stream, &body));
-    lg.kernels = (int)(stats.kernel_launches - before) + 2;
+    lg.kernels = (int)(stats.kernel_launches - before) + 1;
     stats.kernel_launches = before;
     CUDA_OK(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
     return lg;
@@ -1348,7 +1437,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   if (k < 2 || k > cfg.max_chunk) throw HrtError(HRT_ERR_DECODING, "chunk size k not supported by the engine");
   if (b_nat < 1 || b_at < b_nat) throw HrtError(HRT_ERR_DECODING, "need b_at >= b_nat >= 1");
   if (b_at > beam_max) throw HrtError(HRT_ERR_INVALID, "b_at exceeds engine max_beam");
-  if (b_at != 1) throw HrtError(HRT_ERR_INVALID, "fused path: beam search not yet available (use b_at=1)");
+  if (b_at > BEAM_MAX) throw HrtError(HRT_ERR_INVALID, "b_at > 7 unsupported by the device beam search");
+  const int beam = b_at, bn = b_nat;
+  const bool greedy_mode = beam == 1;
   // ---- host schedule: truncate (decoding.py:260), caps, sort by cap desc ----
   std::vector<int> raw_off(B + 1, 0), S(B), cap(B);
   for (int i = 0; i < B; ++i) {
@@ -1364,39 +1455,42 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   std::vector<int> perm(B);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cap[a] > cap[b]; });
-  std::vector<int> off(B + 1, 0), len(B), capS(B), slot(B), off2(B + 1, 0), moff(B + 1, 0);
+  const int C = B * bn;  // Stage-II candidates, c = s * b_nat + i
+  std::vector<int> off(B + 1, 0), len(B), capS(B), slot(C), off2(C + 1, 0), moff(C + 1, 0);
   int max_src = 0, max_cap = 0, max_slot = 0;
   for (int i = 0; i < B; ++i) {
     const int p = perm[i];
     len[i] = S[p];
     off[i + 1] = off[i] + S[p];
     capS[i] = cap[p];
-    slot[i] = k * cap[p];
-    off2[i + 1] = off2[i] + slot[i];
-    moff[i + 1] = moff[i] + (slot[i] - slot[i] / k);
     max_src = std::max(max_src, S[p]);
     max_cap = std::max(max_cap, cap[p]);
-    max_slot = std::max(max_slot, slot[i]);
+  }
+  for (int c = 0; c < C; ++c) {
+    slot[c] = k * capS[c / bn];
+    off2[c + 1] = off2[c] + slot[c];
+    moff[c + 1] = moff[c] + (slot[c] - slot[c] / k);
+    max_slot = std::max(max_slot, slot[c]);
   }
   const int Mtok = off[B];
   if (Mtok > Me_max) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed max_src_tokens");
-  const int M2 = off2[B], Mm = moff[B];
+  const int M2 = off2[C], Mm = moff[C];
   if (M2 > M2_max) throw HrtError(HRT_ERR_MEMORY, "stage-II rows exceed capacity");
-  // rows alive at step t: prefix of the cap-sorted batch
+  // Stage-I rows alive at step t: beam rows of every sentence whose cap > t
+  // (a prefix of the cap-sorted batch)
   std::vector<int> alive(max_cap, 0);
   for (int t = 0, r = B; t < max_cap; ++t) {
     while (r > 0 && capS[r - 1] <= t) --r;
-    alive[t] = r;
+    alive[t] = r * beam;
   }
   // mask-row map for the final Stage-II LayerNorm gather
-  std::vector<int> out_row(M2, -1), seqmap(B), cand_beg(B + 1);
-  for (int i = 0; i < B; ++i) {
-    for (int j = 0; j < slot[i]; ++j)
-      if ((j + 1) % k != 0) out_row[off2[i] + j] = moff[i] + j - (j + 1) / k;
-    seqmap[i] = i;
-    cand_beg[i] = i;
+  std::vector<int> out_row(M2, -1), seqmap(C), cand_beg(B + 1);
+  for (int c = 0; c < C; ++c) {
+    for (int j = 0; j < slot[c]; ++j)
+      if ((j + 1) % k != 0) out_row[off2[c] + j] = moff[c] + j - (j + 1) / k;
+    seqmap[c] = c / bn;
   }
-  cand_beg[B] = B;
+  for (int s = 0; s <= B; ++s) cand_beg[s] = s * bn;
   meta_reset();
   size_t cur = meta_hdr;
   int* d_rawoff = meta_put(cur, raw_off);
@@ -1409,7 +1503,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   int* d_moff = meta_put(cur, moff);
   int* d_seqmap = meta_put(cur, seqmap);
   int* d_cbeg = meta_put(cur, cand_beg);
-  int* d_qlen2 = meta_put(cur, std::vector<int>(B, 0));
+  int* d_qlen2 = meta_put(cur, std::vector<int>(C, 0));
   int* d_outrow = meta_put(cur, out_row);
   const std::vector<int> enc_items = prefill_items(len), s2_items = prefill_items(slot);
   int* d_enc_items = meta_put(cur, enc_items);
@@ -1439,19 +1533,28 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   phase_mark(0);
   run_encoder(Mtok, B, max_src, d_off, d_len, d_enc_items, (int)enc_items.size() / 2);
   phase_mark(1);
-  // ---- phase 2: Stage I (greedy; decoding.py:90-155 with beam = 1) ----
+  // ---- phase 2: Stage I (decoding.py:90-155) ----
   // cache capacity max_steps + 1 (start_cache, decoding.py:97); the fused path
   // keeps the engine-wide stride cap_max so captured graphs stay valid
   const int capA = cap_max;
-  {
-    Scope sc(this, K_OTHER, 0, 0);
-    launch(stage1_init_kernel, cdiv(B, 128), 128, 0, B, capA, 4 + (k - 2) /*BOS_k*/, s_feed, s_done, s_nsteps,
-                                                        s_forced, s_score, s_hist);
-    check_launch();
-  }
+  const int bos = 4 + (k - 2);  // BOS_k (data.py:16)
   CUDA_OK(cudaMemcpyAsync(s_caps, d_caps, B * sizeof(int), cudaMemcpyDeviceToDevice, stream));
   GreedyState gs{E, pe, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, emb_scale, d,
                  s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
+  BeamState bs = beam_state(beam, bn);
+  {
+    Scope sc(this, K_OTHER, 0, 0);
+    if (greedy_mode)
+      launch(stage1_init_kernel, cdiv(B, 128), 128, 0, B, capA, bos, s_feed, s_done, s_nsteps, s_forced, s_score,
+             s_hist);
+    else
+      launch(beam_init_kernel, cdiv(B * beam, 128), 128, 0, bs, B, bos);
+    check_launch();
+    if (!greedy_mode) {
+      launch(rowseq_fill_kernel, cdiv(B * beam, 128), 128, 0, s_rowseq, B * beam, beam);
+      check_launch();
+    }
+  }
   {  // step-0 input (BOS_k at position 0); later steps are embedded by the selection kernel
     Tag _tg(this, "s1.embed_ln");
     embed_ln(s_feed, nullptr, 0, alive.empty() ? 0 : alive[0], dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
@@ -1459,41 +1562,41 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   if (BF16 && use_graphs && timed_class == 0) {
     // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
     int bucket = 1;
-    while (bucket < B) bucket <<= 1;
+    while (bucket < B * beam) bucket <<= 1;
     bucket = std::min(bucket, R_max);
-    LoopGraph& lg = loop_graph(bucket, gs);
+    LoopGraph& lg = loop_graph(bucket, beam, gs, bs);
     CUDA_OK(cudaGraphLaunch(lg.exec, stream));
     stats.kernel_launches += (int64_t)lg.kernels * max_cap;
   } else {
     for (int t = 0; t < max_cap; ++t) {
       const int R = alive[t];
       if (R == 0) break;
-      decoder_step(R, t, t * k, capA, s_feed, s_hist, nullptr, d_off, d_len, max_src, nullptr, false);
-      {
-        Tag _tg(this, "s1.vocab");
-        vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits);
-      }
-      Tag _tg(this, "s1.select");
-      Scope sc(this, K_OTHER, 0, 0);
-      launch(greedy_select_kernel<T, 1>, cdiv(R, 4), 128, 0, s1.parts, gs, R, t, k, nullptr);
-      check_launch();
+      stage1_step(R, t, k, beam, max_src, d_off, d_len, gs, bs, nullptr);
     }
   }
   phase_mark(2);
-  // ---- phase 3: Stage II over the greedy chain (b_nat = 1) ----
+  // ---- phase 3: Stage II over the selected candidates ----
+  Stage2Cands cands;
+  if (greedy_mode) {
+    cands = Stage2Cands{s_anchors, nullptr, capA, s_nsteps, s_score, s_forced, s_nsteps};
+  } else {
+    Scope sc(this, K_OTHER, 0, 0);
+    launch(beam_candidates_kernel, cdiv(B, 128), 128, 0, bs, B, c_off, c_len, c_sat, c_forced);
+    check_launch();
+    cands = Stage2Cands{b_ftok, c_off, capA, c_len, c_sat, c_forced, bs.nsteps};
+  }
   {
     Scope sc(this, K_OTHER, 0, 0);
-    launch(stage2_build_kernel, B, 128, 0, s_anchors, capA, d_seqmap, s_nsteps, d_off2, d_slot, B, k, s2.ids,
-                                               s2.pos, d_qlen2);
+    launch(stage2_build_kernel, C, 128, 0, cands, d_off2, d_slot, C, k, s2.ids, s2.pos, d_qlen2);
     check_launch();
   }
-  decoder_parallel(M2, B, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
+  decoder_parallel(M2, C, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
                    d_s2_items, (int)s2_items.size() / 2);
   Tag _tg2(this, "stage2.vocab");
   vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
   {
     Scope sc(this, K_OTHER, 0, 0);
-    launch(rowstat_kernel<1>, cdiv(Mm, 4), 128, 0, s2.parts, Mm, 1, s2.mstat);
+    launch(rowstat_kernel<1>, cdiv(Mm, 4), 128, 0, s2.parts, Mm, 1, s2.mstat, (const int*)nullptr);
     check_launch();
   }
   Stage2Out so;
@@ -1505,8 +1608,8 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   so.out_index = d_perm;
   {
     Scope sc(this, K_OTHER, 0, 0);
-    launch(stage2_finish_kernel, cdiv(B, 4), 128, 0, s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, d_seqmap,
-                                                        s_score, s_nsteps, s_forced, k, alpha, Lmax, B, so);
+    launch(stage2_finish_kernel, cdiv(B, 4), 128, 0, s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, cands, k,
+           alpha, Lmax, B, so);
     check_launch();
   }
   phase_mark(3);
@@ -1520,8 +1623,6 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     CUDA_OK(cudaStreamSynchronize(stream));
     for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
   }
-  size_t hw = 0;
-  (void)hw;
 }
 
 }  // namespace hrt

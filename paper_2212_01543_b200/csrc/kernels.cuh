@@ -495,8 +495,9 @@ __global__ void __launch_bounds__(AM_WARPS * 32) attn_prefill_mma_kernel(
 template <typename T, int DH, bool SELF>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const T* __restrict__ q, int q_stride, const T* __restrict__ knew, const T* __restrict__ vnew, int new_stride,
-    T* __restrict__ kc, T* __restrict__ vc, int c_stride, const int* __restrict__ hist, int cap, int t,
-    const int* __restrict__ t_dev, const int* __restrict__ row_seq, const int* __restrict__ kv_off,
+    T* __restrict__ kc, T* __restrict__ vc, int c_stride, const int* __restrict__ hist_a,
+    const int* __restrict__ hist_b, int cap, int t, const int* __restrict__ t_dev, const int* __restrict__ row_seq,
+    const int* __restrict__ kv_off,
     const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale,
     T* __restrict__ out, int out_stride) {
   pdl_enter();
@@ -504,6 +505,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;
   if (R_dev) R = *R_dev;
   if (t_dev) t = *t_dev;
+  // beam decoding ping-pongs the history map by step parity (reorder writes the other one)
+  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * nwarp + warp;
   if (item >= R * heads) return;
@@ -1013,8 +1016,10 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
 
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.
 template <int KT>
-__global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restrict__ out) {
+__global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restrict__ out,
+                               const int* __restrict__ R_dev = nullptr) {
   pdl_enter();
+  if (R_dev) R = *R_dev;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= R) return;
   const RowStat rs = merge_row<KT>(parts, row, kt);
@@ -1027,17 +1032,27 @@ __global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restr
 // position j < k*m holds MASK, or the anchor z_{(j+1)/k-1} when (j+1) % k == 0;
 // positions are j + 1. Rows past k*m are padding (never attended, ignored).
 // ---------------------------------------------------------------------------
-__global__ void stage2_build_kernel(const int* __restrict__ anchors, int cap, const int* __restrict__ cand_row,
-                                    const int* __restrict__ cand_len, const int* __restrict__ off,
-                                    const int* __restrict__ slot, int C, int k, int* __restrict__ ids,
-                                    int* __restrict__ pos, int* __restrict__ qlen) {
+// Stage-II candidates: anchors of candidate c live at tok + (tok_off ?
+// tok_off[c] : c * cap), len[c] anchors (0 = no such candidate).
+struct Stage2Cands {
+  const int* tok;
+  const int* tok_off;
+  int cap;
+  const int* len;
+  const double* s_at;  // [C] Stage-I score of the candidate
+  const int* forced;   // [C]
+  const int* steps;    // [S] Stage-I steps of the sentence
+};
+
+__global__ void stage2_build_kernel(Stage2Cands cands, const int* __restrict__ off, const int* __restrict__ slot, int C,
+                                    int k, int* __restrict__ ids, int* __restrict__ pos, int* __restrict__ qlen) {
   pdl_enter();
   const int c = blockIdx.x;
   if (c >= C) return;
-  const int m = cand_len[c];
+  const int m = cands.len[c];
   const int T = k * m;
   const int sl = slot[c], o = off[c];
-  const int* z = anchors + (size_t)cand_row[c] * cap;
+  const int* z = cands.tok + (cands.tok_off ? (size_t)cands.tok_off[c] : (size_t)c * cands.cap);
   if (threadIdx.x == 0) qlen[c] = T;
   for (int j = threadIdx.x; j < sl; j += blockDim.x) {
     int id = PAD_ID;
@@ -1068,9 +1083,7 @@ struct Stage2Out {
 __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __restrict__ off,
                                      const int* __restrict__ qlen, const int* __restrict__ mrow_off,
                                      const RowStat* __restrict__ mstat, const int* __restrict__ cand_beg,
-                                     const int* __restrict__ cand_row, const double* __restrict__ s_at,
-                                     const int* __restrict__ nsteps, const int* __restrict__ forced, int k,
-                                     float alpha, int max_len, int S, Stage2Out out) {
+                                     Stage2Cands cands, int k, float alpha, int max_len, int S, Stage2Out out) {
   pdl_enter();
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1079,6 +1092,7 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
   double best_score = 0.0, best_cmlm = 0.0;
   for (int c = cand_beg[s]; c < cand_beg[s + 1]; ++c) {
     const int T = qlen[c];
+    if (T == 0) continue;  // no such candidate
     const int o = off[c];
     double part = 0.0;
     // MASK positions j (in slot layout) map to consecutive stat rows
@@ -1092,7 +1106,7 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
     }
     (void)o;
     const double cmlm = warp_sum_d(part);
-    const double sc = (s_at[cand_row[c]] + cmlm) / pow((double)T, (double)alpha);
+    const double sc = (cands.s_at[c] + cmlm) / pow((double)T, (double)alpha);
     if (best < 0 || sc > best_score) {
       best = c;
       best_score = sc;
@@ -1126,13 +1140,312 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
     out.tokens[(size_t)dst * max_len + j] = tok;
   }
   if (lane == 0) {
-    const int r = cand_row[c];
     out.lens[dst] = n;
-    out.scores[(size_t)dst * 3 + 0] = s_at[r];
+    out.scores[(size_t)dst * 3 + 0] = cands.s_at[c];
     out.scores[(size_t)dst * 3 + 1] = best_cmlm;
     out.scores[(size_t)dst * 3 + 2] = best_score;
-    out.calls[dst] = nsteps[r] + 1;
-    out.forced[dst] = (unsigned char)forced[r];
+    out.calls[dst] = cands.steps[s] + 1;
+    out.forced[dst] = (unsigned char)cands.forced[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage-I beam search on device (decoding.py:90-155, b_at > 1).
+// Sentence s owns rows [s*beam, (s+1)*beam); row s*beam + h holds live
+// hypothesis h. One warp per sentence per step:
+//   1. candidates: every live hypothesis contributes its top (beam+1)
+//      generable tokens (or EOS at the cap), score += fp32 log-prob in fp64;
+//   2. stable sort by (-score, token) -- warp-parallel rank counting with the
+//      generation index as the final tie break (Python's stable sort);
+//   3. lane 0 applies the acceptance rules: EOS finishes if rank < beam or
+//      greedy; others fill new_live up to beam; greedy-chain reservation;
+//      break when nothing is live or (>= beam finished and greedy done);
+//   4. the warp reorders the rows (anchor history + KV history index map,
+//      ping-pong buffers by step parity) and embeds the next step's inputs.
+// Finished hypotheses: a per-sentence top-b_nat list (stable by -score) plus
+// the greedy one, in a (b_nat + 2)-slot token pool.
+// ---------------------------------------------------------------------------
+constexpr int BEAM_MAX = 7, BEAM_MAXC = BEAM_MAX * (BEAM_MAX + 1);
+
+struct BeamState {
+  int beam, bnat, cap;
+  int* feed;         // [rows]
+  double* score;     // [rows]
+  int* greedy;       // [rows]
+  int* anchors[2];   // [rows][cap] ping-pong
+  int* hist[2];      // [rows][cap] ping-pong
+  int* live_n;       // [S]
+  int* done;         // [S]
+  int* nsteps;       // [S]
+  int* n_fin;        // [S]
+  int* greedy_done;  // [S]
+  const int* caps;   // [S]
+  // finished store, F = bnat + 2 slots per sentence
+  int* f_count;      // [S] entries in the top list
+  int* f_list;       // [S][bnat] slot of the i-th best
+  int* f_gslot;      // [S] slot of the finished greedy hypothesis (-1: none)
+  double* f_score;   // [S][F]
+  int* f_len;        // [S][F]
+  int* f_forced;     // [S][F]
+  int* f_tok;        // [S][F][cap]
+  // next-step embedding
+  const void* E;
+  const float* pe;
+  const float* ln_g;
+  const float* ln_b;
+  float* x;
+  void* y;
+  float scale;
+  int d;
+};
+
+__global__ void beam_init_kernel(BeamState st, int S, int bos) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = S * st.beam;
+  if (i < rows) {
+    st.feed[i] = bos;
+    st.score[i] = 0.0;
+    st.greedy[i] = (i % st.beam) == 0;
+    for (int j = 0; j < st.cap; ++j) st.hist[0][(size_t)i * st.cap + j] = i;
+  }
+  if (i < S) {
+    st.live_n[i] = 1;
+    st.done[i] = 0;
+    st.nsteps[i] = 0;
+    st.n_fin[i] = 0;
+    st.greedy_done[i] = 0;
+    st.f_count[i] = 0;
+    st.f_gslot[i] = -1;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) beam_select_kernel(const RowStat* __restrict__ rs, BeamState st, int S, int t,
+                                                          int k, StepCtl* ctl) {
+  pdl_enter();
+  __shared__ double cs[4][BEAM_MAXC];
+  __shared__ int ct[4][BEAM_MAXC], cp[4][BEAM_MAXC], cg[4][BEAM_MAXC], ord[4][BEAM_MAXC];
+  __shared__ int nl_s[4], brk_s[4], ntok[4][BEAM_MAX], npar[4][BEAM_MAX], ncopy[4], copy_slot[4][BEAM_MAXC],
+      copy_src[4][BEAM_MAXC];
+  const int beam = st.beam;
+  if (ctl) {
+    S = ctl->R / beam;
+    t = ctl->t;
+    k = ctl->k;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (blockDim.x >> 5) + w;
+  if (s >= S) return;
+  const int r0 = s * beam;
+  const int cur = t & 1, nxt = cur ^ 1;
+  const int cap = st.cap;
+  const int F = st.bnat + 2;
+  if (!st.done[s]) {
+    const int L = st.live_n[s];
+    const bool last = (t == st.caps[s] - 1);
+    const int nt = last ? 1 : beam + 1;
+    const int n = L * nt;
+    // 1. candidates in generation order (parent-major, then rank in the row's top list)
+    for (int i = lane; i < n; i += 32) {
+      const int h = i / nt, q = i - h * nt;
+      const RowStat& R = rs[r0 + h];
+      int g = R.id[0];
+      if (g == 0x7fffffff) g = EOS_ID;
+      int tok;
+      float logit;
+      if (last) {
+        tok = EOS_ID;
+        logit = R.eos;
+      } else {
+        tok = R.id[q];
+        logit = R.val[q];
+        if (tok == 0x7fffffff) {  // fewer generable ids than beam + 1: never selectable
+          tok = EOS_ID;
+          logit = -INFINITY;
+        }
+      }
+      const float lp = (logit - R.mx) - R.lse;
+      cs[w][i] = st.score[r0 + h] + (double)lp;
+      ct[w][i] = tok;
+      cp[w][i] = h;
+      cg[w][i] = st.greedy[r0 + h] && (last || tok == g);
+    }
+    __syncwarp();
+    // 2. stable rank by (-score, token, generation index)
+    for (int i = lane; i < n; i += 32) {
+      const double si = cs[w][i];
+      const int ti = ct[w][i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const double sj = cs[w][j];
+        const int tj = ct[w][j];
+        rank += (sj > si) || (sj == si && (tj < ti || (tj == ti && j < i)));
+      }
+      ord[w][rank] = i;
+    }
+    __syncwarp();
+    // 3. acceptance rules (lane 0, sequential in rank order)
+    if (lane == 0) {
+      int nl = 0, nc = 0;
+      bool gdone = st.greedy_done[s] != 0;
+      int* flist = st.f_list + (size_t)s * st.bnat;
+      auto finish = [&](int i) {
+        const bool g = cg[w][i] != 0;
+        st.n_fin[s] += 1;
+        const double sc = cs[w][i];
+        // stable insert position in the top-b_nat list (after equal scores)
+        int cnt = st.f_count[s];
+        int p = cnt;
+        for (int a = 0; a < cnt; ++a)
+          if (st.f_score[(size_t)s * F + flist[a]] < sc) {
+            p = a;
+            break;
+          }
+        const bool top = p < st.bnat;
+        if (!top && !g) return;
+        // free slot: referenced neither by the top list nor by the greedy pointer
+        int slot = -1;
+        for (int q = 0; q < F && slot < 0; ++q) {
+          bool used = (st.f_gslot[s] == q);
+          for (int a = 0; a < cnt && !used; ++a) used = flist[a] == q;
+          if (!used) slot = q;
+        }
+        st.f_score[(size_t)s * F + slot] = sc;
+        st.f_len[(size_t)s * F + slot] = t + 1;
+        st.f_forced[(size_t)s * F + slot] = last ? 1 : 0;
+        copy_slot[w][nc] = slot;
+        copy_src[w][nc] = r0 + cp[w][i];
+        ++nc;
+        if (top) {
+          const int newcnt = cnt < st.bnat ? cnt + 1 : st.bnat;
+          for (int a = newcnt - 1; a > p; --a) flist[a] = flist[a - 1];
+          flist[p] = slot;
+          st.f_count[s] = newcnt;
+        }
+        if (g) {
+          st.f_gslot[s] = slot;
+          gdone = true;
+        }
+      };
+      for (int rank = 0; rank < n; ++rank) {
+        const int i = ord[w][rank];
+        if (ct[w][i] == EOS_ID) {
+          if (rank < beam || cg[w][i]) finish(i);
+        } else if (nl < beam) {
+          ntok[w][nl] = i;
+          ++nl;
+        }
+      }
+      if (!gdone) {
+        bool any = false;
+        for (int a = 0; a < nl; ++a) any |= cg[w][ntok[w][a]] != 0;
+        if (!any && nl > 0) {
+          for (int rank = 0; rank < n; ++rank) {
+            const int i = ord[w][rank];
+            if (cg[w][i] && ct[w][i] != EOS_ID) {
+              ntok[w][nl - 1] = i;
+              break;
+            }
+          }
+        }
+      }
+      st.greedy_done[s] = gdone;
+      const bool brk = nl == 0 || (st.n_fin[s] >= beam && gdone);
+      if (brk) {
+        st.done[s] = 1;
+        st.nsteps[s] = t + 1;
+        if (ctl) atomicAdd(&ctl->finished, 1);
+      }
+      for (int a = 0; a < nl; ++a) npar[w][a] = cp[w][ntok[w][a]];
+      nl_s[w] = nl;
+      brk_s[w] = brk;
+      ncopy[w] = nc;
+    }
+    __syncwarp();
+    // finished token copies: parent history + EOS
+    for (int c = 0; c < ncopy[w]; ++c) {
+      int* dst = st.f_tok + ((size_t)s * F + copy_slot[w][c]) * cap;
+      const int* src = st.anchors[cur] + (size_t)copy_src[w][c] * cap;
+      for (int j = lane; j <= t; j += 32) dst[j] = (j < t) ? src[j] : EOS_ID;
+    }
+    // 4. reorder into the next buffers (rows past nl continue from row 0, decoding.py:151)
+    if (!brk_s[w]) {
+      const int nl = nl_s[w];
+      for (int j = 0; j < beam; ++j) {
+        const int par = j < nl ? npar[w][j] : 0;
+        const int src = r0 + par, dst = r0 + j;
+        const int* ah = st.anchors[cur] + (size_t)src * cap;
+        int* an = st.anchors[nxt] + (size_t)dst * cap;
+        const int* hh = st.hist[cur] + (size_t)src * cap;
+        int* hn = st.hist[nxt] + (size_t)dst * cap;
+        const int tok = j < nl ? ct[w][ntok[w][j]] : st.feed[dst];
+        for (int q = lane; q <= t; q += 32) {
+          an[q] = (q < t) ? ah[q] : tok;
+          hn[q] = (q < t) ? hh[q] : src;  // slot t was appended by physical row src
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int j = 0; j < nl; ++j) {
+          const int i = ntok[w][j];
+          st.score[r0 + j] = cs[w][i];
+          st.greedy[r0 + j] = cg[w][i];
+          st.feed[r0 + j] = ct[w][i];
+        }
+        for (int j = nl; j < beam; ++j) st.greedy[r0 + j] = 0;
+        st.live_n[s] = nl;
+      }
+    }
+  }
+  __syncwarp();
+  // next step's embedding for all rows of the sentence (finished ones feed stale tokens)
+  if (st.x != nullptr) {
+    for (int j = 0; j < beam; ++j) {
+      const int r = r0 + j;
+      const int tok = st.feed[r];
+      warp_embed_ln<T>(static_cast<const T*>(st.E), st.pe, st.ln_g, st.ln_b, st.scale, st.d, tok, (t + 1) * k,
+                       st.x + (size_t)r * st.d, static_cast<T*>(st.y) + (size_t)r * st.d);
+    }
+  }
+}
+
+// Stage-II candidates of every sentence (decoding.py:262-266): the top-b_nat
+// finished hypotheses by score (stable), the greedy one forced into the last
+// place when missing. Candidate c = s * b_nat + i.
+__global__ void beam_candidates_kernel(BeamState st, int S, int* __restrict__ c_off, int* __restrict__ c_len,
+                                       double* __restrict__ c_sat, int* __restrict__ c_forced) {
+  pdl_enter();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const int F = st.bnat + 2;
+  const int* flist = st.f_list + (size_t)s * st.bnat;
+  int cnt = st.f_count[s];
+  int sl[8];
+  for (int a = 0; a < cnt; ++a) sl[a] = flist[a];
+  const int g = st.f_gslot[s];
+  if (g >= 0 && cnt > 0) {
+    bool in = false;
+    for (int a = 0; a < cnt; ++a) in |= sl[a] == g;
+    if (!in) sl[cnt - 1] = g;
+  } else if (g >= 0 && cnt == 0) {
+    sl[0] = g;
+    cnt = 1;
+  }
+  for (int a = 0; a < st.bnat; ++a) {
+    const int c = s * st.bnat + a;
+    if (a < cnt) {
+      const int slot = sl[a];
+      c_off[c] = (s * F + slot) * st.cap;
+      c_len[c] = st.f_len[(size_t)s * F + slot];
+      c_sat[c] = st.f_score[(size_t)s * F + slot];
+      c_forced[c] = st.f_forced[(size_t)s * F + slot];
+    } else {
+      c_off[c] = 0;
+      c_len[c] = 0;
+      c_sat[c] = 0.0;
+      c_forced[c] = 0;
+    }
   }
 }
 
@@ -1166,6 +1479,13 @@ __global__ void stage1_init_kernel(int R, int cap, int bos, int* feed, int* done
   forced[r] = 0;
   score[r] = 0.0;
   for (int j = 0; j < cap; ++j) hist[(size_t)r * cap + j] = r;
+}
+
+// Stage-I row -> encoded sentence (beam rows share their sentence's memory)
+__global__ void rowseq_fill_kernel(int* __restrict__ rowseq, int rows, int beam) {
+  pdl_enter();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) rowseq[r] = r / beam;
 }
 
 // Beam reorder as an index permutation (infer.py:307-318): row j continues

@@ -2,10 +2,10 @@
 
 `hrt_translate(session, source, k, ...)` keeps the reference signature. With a
 `CudaSession` it runs the fused device path (`hrt_translate_batch`: encoder,
-Stage-I skip-AT loop, Stage-II fill and Eq.(2) selection all on the GPU).
-Configurations the fused path does not cover yet (Stage-I beam) run the
-protocol-level search below, which drives the same device kernels one decoder
-call at a time through the session protocol.
+Stage-I skip-AT greedy or beam loop, Stage-II fill and Eq.(2) selection all on
+the GPU). With any other object implementing the session protocol (e.g. the
+reference's own session, or a test double) it runs the protocol-level search
+below, one decoder call at a time.
 
 Selection semantics (every rule here is the reference's):
 * Stage-I scores: full-vocabulary log-softmax, excluded ids only barred from
@@ -214,7 +214,7 @@ def hrt_translate(session, source, k, b_at=1, b_nat=1, length_penalty=0.6, ws=No
     if k not in session.config.chunk_sizes:
         raise DecodingError(f"chunk size k={k} not supported by the model")
     t0 = time.perf_counter()
-    if isinstance(session, CudaSession) and b_at == 1:
+    if isinstance(session, CudaSession):
         ms = None if max_steps is None else [int(max_steps)]
         tr = session.translate_batch([list(source)], k, b_at, b_nat, length_penalty, ms)[0]
     else:
@@ -227,7 +227,7 @@ def hrt_translate_batch(session, sources, k, b_at=1, b_nat=1, length_penalty=0.6
     """Batched hrt_translate: one fused device call for the whole batch."""
     if b_nat < 1 or b_at < b_nat:
         raise DecodingError("need b_at >= b_nat >= 1")
-    if isinstance(session, CudaSession) and b_at == 1:
+    if isinstance(session, CudaSession):
         return session.translate_batch(list(map(list, sources)), k, b_at, b_nat, length_penalty, max_steps)
     caps = [None] * len(sources) if max_steps is None else list(max_steps)
     return [hrt_translate(session, s, k, b_at, b_nat, length_penalty, max_steps=m) for s, m in zip(sources, caps)]

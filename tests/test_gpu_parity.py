@@ -168,22 +168,46 @@ def test_c1_first_steps_logp(hrt, golden):
                 int(np.argmax(O.allowed_row(lp)))]
 
 
-@pytest.mark.parametrize("name", ["tiny_trained", "dh64"])
-def test_protocol_beam_matches_golden(hrt, golden, name):
-    """Stage-I beam through the session protocol (device step/reorder kernels)."""
-    g = golden(name)
-    model = _model(hrt, g)
-    sess = hrt.CudaSession(model, dtype=np.float32, max_beam=4)
-    runs = [r for r in g["runs"] if r["b_at"] > 1 and r.get("dtype", "f32") in ("f32", "f64")]
-    seen = set()
-    for r in runs:
-        key = (r["src"], r["k"], r["b_at"], r["b_nat"])
-        if key in seen:
+def _beam_runs(g):
+    runs, seen = [], set()
+    for r in g["runs"]:
+        if r["b_at"] == 1 or r.get("dtype", "f32") not in ("f32", "f64"):
             continue
-        seen.add(key)
-        tr = hrt.hrt_translate(sess, g["sources"][r["src"]], r["k"], r["b_at"], r["b_nat"],
-                               max_steps=r["max_steps"])
+        key = (r["src"], r["k"], r["b_at"], r["b_nat"])
+        if key not in seen:
+            seen.add(key)
+            runs.append(r)
+    return runs
+
+
+@pytest.mark.parametrize("name", ["tiny_trained", "dh64", "toy"])
+def test_protocol_beam_matches_golden(hrt, golden, name):
+    """Stage-I beam through the session protocol (device step/reorder kernels,
+    host-side selection)."""
+    from paper_2212_01543_b200 import decoding as PD
+
+    g = golden(name)
+    sess = hrt.CudaSession(_model(hrt, g), dtype=np.float32, max_beam=4)
+    for r in _beam_runs(g)[::2]:
+        tr = PD._protocol_translate(sess, g["sources"][r["src"]], r["k"], r["b_at"], r["b_nat"], 0.6,
+                                    r["max_steps"])
         _check_translation(tr, r["out"])
+
+
+@pytest.mark.parametrize("name", ["tiny_trained", "dh64", "toy"])
+def test_fused_beam_matches_golden(hrt, golden, name):
+    """Device beam search (b_at > 1) + multi-candidate Stage II (b_nat > 1), one
+    fused batch per (k, b_at, b_nat) group."""
+    g = golden(name)
+    sess = hrt.CudaSession(_model(hrt, g), dtype=np.float32, max_beam=4, max_sentences=len(g["sources"]))
+    groups = {}
+    for r in _beam_runs(g):
+        groups.setdefault((r["k"], r["b_at"], r["b_nat"], r["max_steps"] is None), []).append(r)
+    for (k, b_at, b_nat, uncapped), rs in groups.items():
+        caps = None if uncapped else [r["max_steps"] for r in rs]
+        out = hrt.hrt_translate_batch(sess, [g["sources"][r["src"]] for r in rs], k, b_at, b_nat, max_steps=caps)
+        for tr, r in zip(out, rs):
+            _check_translation(tr, r["out"])
 
 
 def test_bf16_token_agreement(hrt, golden):
@@ -253,3 +277,19 @@ def test_graph_loop_equals_eager(hrt, golden):
         for x, y in zip(a, b):
             assert x.tokens == y.tokens
             assert x.score == y.score and x.decoder_calls == y.decoder_calls
+
+
+def test_fused_beam_bf16_graph_equals_eager(hrt, golden):
+    g = golden("dh64")
+    eng = hrt.Engine(_model(hrt, g), dtype="bfloat16", max_sentences=16, max_beam=4)
+    from paper_2212_01543_b200 import workload as W
+
+    srcs = W.make_sources(13, 9, ("uniform", 3, 40), vocab_size=1000)
+    caps = W.stage1_caps(srcs, 2)
+    for b_at, b_nat in ((4, 1), (4, 4), (2, 2)):
+        eng.set_option("graphs", 1)
+        a = eng.translate_batch(srcs, 2, b_at, b_nat, max_steps=caps)
+        eng.set_option("graphs", 0)
+        b = eng.translate_batch(srcs, 2, b_at, b_nat, max_steps=caps)
+        for x, y in zip(a, b):
+            assert x.tokens == y.tokens and x.score == y.score and x.decoder_calls == y.decoder_calls
