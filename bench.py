@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--beam", type=int, default=None, help="Stage-I beam b_at (default: the config's)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-batch1", action="store_true")
@@ -63,7 +64,9 @@ def dist_env():
 def workload(args, rank, step):
     from paper_2212_01543_b200 import workload as W
 
-    spec = W.CONFIGS[args.config]
+    spec = dict(W.CONFIGS[args.config])
+    if args.beam:
+        spec["beam"] = args.beam
     k = args.k or spec["k"]
     # inputs seed = weight seed + 1000; ranks/steps get disjoint streams
     seed = spec["seed"] + 1000 + 7919 * rank + 104729 * step
@@ -149,7 +152,7 @@ def make_oracle(spec):
     return O.Oracle(ocfg, params, dtype=np.float32)
 
 
-def oracle_decode(orc, k, srcs, caps, budget_s=None):
+def oracle_decode(orc, k, srcs, caps, budget_s=None, b_at=1):
     """Sequential per-sentence decode (the reference has no batched path):
     all of srcs, or as many as fit in budget_s seconds (at least 3)."""
     from oracle import hrt_oracle as O
@@ -157,7 +160,7 @@ def oracle_decode(orc, k, srcs, caps, budget_s=None):
     words = n = 0
     t0 = time.monotonic()
     while n < len(srcs) and (budget_s is None or n < 3 or time.monotonic() - t0 < budget_s):
-        words += len(O.hrt_translate(orc, srcs[n], k, max_steps=caps[n]).tokens)
+        words += len(O.hrt_translate(orc, srcs[n], k, b_at=b_at, b_nat=1, max_steps=caps[n]).tokens)
         n += 1
     return n, words, time.monotonic() - t0
 
@@ -166,8 +169,8 @@ def cpu_reference(spec, k, srcs, caps, budget_s):
     """cpu_baseline leg: the oracle port (fp32 numpy, all host BLAS threads)
     on a bounded sample of the step batch."""
     orc = make_oracle(spec)
-    oracle_decode(orc, k, srcs[:1], caps[:1])  # warm-up (measure_wps protocol, bench.py:81-82)
-    n, words, dt = oracle_decode(orc, k, srcs, caps, budget_s)
+    oracle_decode(orc, k, srcs[:1], caps[:1], b_at=spec["beam"])  # warm-up (measure_wps protocol, bench.py:81-82)
+    n, words, dt = oracle_decode(orc, k, srcs, caps, budget_s, b_at=spec["beam"])
     return dict(value=words / dt, unit=UNIT, cores=len(os.sched_getaffinity(0)), kind="port",
                 sample=f"first {n} sentences of the step batch ({words} target words), decoded sequentially by "
                        f"the fp32 numpy oracle port (oracle/hrt_oracle.py) in {dt:.1f} s")
@@ -182,11 +185,11 @@ def run_reference(args):
     per_step = max(1, int(os.environ.get("HRT_REF_SENTENCES", "4")))
     orc = make_oracle(spec)
     for s in range(args.warmup):  # untimed warm-up steps (one sentence each)
-        oracle_decode(orc, k, srcs[s: s + 1], caps[s: s + 1])
+        oracle_decode(orc, k, srcs[s: s + 1], caps[s: s + 1], b_at=spec["beam"])
     times, words = [], 0
     for s in range(args.steps):
         lo = (args.warmup + s * per_step) % max(1, len(srcs) - per_step)
-        n, w, dt = oracle_decode(orc, k, srcs[lo: lo + per_step], caps[lo: lo + per_step])
+        n, w, dt = oracle_decode(orc, k, srcs[lo: lo + per_step], caps[lo: lo + per_step], b_at=spec["beam"])
         times.append(dt)
         words += w
     val = words / sum(times)
@@ -223,8 +226,9 @@ def run_engine(args):
     sh = spec["shape"]
     B = args.batch
     model = hrt.HRTModel.random(sh, spec["seed"])
+    b_at = spec["beam"]
     eng = hrt.Engine(model, dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", device=local,
-                     max_sentences=B, max_beam=1)
+                     max_sentences=B, max_beam=b_at)
     del model
 
     batches = [workload(args, rank, s) for s in range(args.warmup + args.steps)]
@@ -257,7 +261,7 @@ def run_engine(args):
         e0, e1 = ev(), ev()
         n0 = eng.stats()["kernel_launches"]
         e0.record(stream)
-        eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps)
+        eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps)
         e1.record(stream)
         e1.synchronize()
         n1 = eng.stats()["kernel_launches"]
@@ -280,7 +284,7 @@ def run_engine(args):
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
         e0.record(stream)
-        eng.translate_arrays(ids_h, lens, k=k, max_steps=caps, out=hout)
+        eng.translate_arrays(ids_h, lens, k=k, b_at=b_at, max_steps=caps, out=hout)
         e1.record(stream)
         e1.synchronize()
         h2d = ids_h.nbytes + lens.nbytes
@@ -352,14 +356,14 @@ def run_engine(args):
         ids1 = [np.asarray(s, np.int32) for s in srcs[:n1]]
         out1 = eng.alloc_outputs(1, pinned=pin)
         for i in range(3):
-            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, max_steps=[caps[i]], out=out1)
+            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, b_at=b_at, max_steps=[caps[i]], out=out1)
         e0, e1 = ev(), ev()
         torch.cuda.synchronize()
         w1 = 0
         e0.record(stream)
         t0 = time.perf_counter()
         for i in range(n1):
-            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, max_steps=[caps[i]], out=out1)
+            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, b_at=b_at, max_steps=[caps[i]], out=out1)
             w1 += int(out1["lens"][0])
         e1.record(stream)
         e1.synchronize()
@@ -377,11 +381,11 @@ def run_engine(args):
             ids = torch.tensor(np.concatenate([np.asarray(s, np.int32) for s in srcs[:bs]]), device="cuda")
             lens = np.array([len(s) for s in srcs[:bs]], np.int32)
             for _ in range(2):
-                eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps[:bs])
+                eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps[:bs])
             torch.cuda.synchronize()
             e0, e1 = ev(), ev()
             e0.record(stream)
-            eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, max_steps=caps[:bs])
+            eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps[:bs])
             e1.record(stream)
             e1.synchronize()
             ms = e0.elapsed_time(e1)
@@ -410,8 +414,9 @@ def run_engine(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": spec["dtype"], "data": "synthetic",
-        "config": {"workload": f"{args.config}: HRT k={k} greedy, E{sh.enc_layers}D{sh.dec_layers} d{sh.d_model} "
-                               f"V{sh.vocab_size}, batch {B} sentences/GPU/step, log-normal lengths mean 28, "
+        "config": {"workload": f"{args.config}: HRT k={k} {'greedy' if b_at == 1 else f'beam {b_at} (b_nat 1)'}, "
+                               f"E{sh.enc_layers}D{sh.dec_layers} d{sh.d_model} "
+                               f"V{sh.vocab_size}, batch {B} sentences/GPU/step, lengths {spec['lengths']}, "
                                f"Zipf(1.1) ids, random N(0,0.02) weights seed {spec['seed']}",
                    "batch_per_gpu": B, "k": k, "l2": "512 MiB flush between timed steps (outside events)",
                    "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"},

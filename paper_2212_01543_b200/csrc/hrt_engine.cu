@@ -294,6 +294,8 @@ struct Engine : EngineBase {
     cudaFree(arena);
     cudaFree(p_logits);
     cudaFree(p_mem);
+    cudaFree(sk_ws);
+    cudaFree(sk_counters);
     if (h_meta) cudaFreeHost(h_meta);
     for (auto& kv : loop_graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -491,7 +493,8 @@ struct Engine : EngineBase {
   // vocab GEMM tile width: 256 whenever the vocabulary is large (fewer
   // partials per row for the selection merge, one tile per CTA at small R)
   int vocab_bn(int rows) const { return V >= 4096 ? 256 : choose_bn(rows, V); }
-  int nt_for_rows(int rows) const { return BF16 ? cdiv(V, vocab_bn(rows)) : cdiv(V, 256); }
+  // upper bound on vocab tiles per row for any row count (partials sizing)
+  int nt_bound() const { return (BF16 && V < 4096) ? cdiv(V, 64) : cdiv(V, 256); }
 
   void carve(int phase, Plan& p, char* base) {
     if (phase == 0) {
@@ -509,7 +512,7 @@ struct Engine : EngineBase {
       s1.hid = p.take<T>(base, (size_t)R_max * ff);
       s1.kc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
       s1.vc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
-      const size_t ntot = (size_t)std::max(R_max * nt_for_rows(R_max), std::min(R_max, 128) * nt_max);
+      const size_t ntot = (size_t)R_max * nt_bound();
       s1.parts.mx = p.take<float>(base, ntot);
       s1.parts.sum = p.take<float>(base, ntot);
       s1.parts.val = p.take<float>(base, ntot * KTOP_MAX);
@@ -528,7 +531,7 @@ struct Engine : EngineBase {
       s2.ids = p.take<int>(base, M2_max);
       s2.pos = p.take<int>(base, M2_max);
       s2.out_row = p.take<int>(base, M2_max);
-      const size_t ntot = (size_t)std::max(Mm_max * nt_for_rows(Mm_max), std::min(Mm_max, 128) * nt_max);
+      const size_t ntot = (size_t)Mm_max * nt_bound();
       s2.parts.mx = p.take<float>(base, ntot);
       s2.parts.sum = p.take<float>(base, ntot);
       s2.parts.val = p.take<float>(base, ntot);  // KT = 1 in Stage II
@@ -610,6 +613,11 @@ struct Engine : EngineBase {
       carve(ph, p, arena);
     }
     stats.arena_bytes = (int64_t)(arena_bytes + pbytes);
+    if (BF16) {
+      CUDA_OK(cudaMalloc(&sk_ws, sk_ws_bytes));
+      CUDA_OK(cudaMalloc(&sk_counters, sk_max_tiles * sizeof(int)));
+      CUDA_OK(cudaMemset(sk_counters, 0, sk_max_tiles * sizeof(int)));
+    }
     CUDA_OK(cudaMallocHost(&h_meta, (size_t)meta_cap * sizeof(int)));
     CUDA_OK(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming));
     CUDA_OK(cudaEventRecord(meta_ev, stream));
@@ -625,6 +633,23 @@ struct Engine : EngineBase {
     return tmaps.emplace(key, make_tmap_bf16_kmajor(p, rows, cols, ld, box)).first->second;
   }
 
+  // split-K workspace: fp32 partial tiles + per-tile arrival counters
+  float* sk_ws = nullptr;
+  int* sk_counters = nullptr;
+  size_t sk_ws_bytes = (size_t)64 << 20;
+  int sk_max_tiles = 16384;
+  bool use_splitk = false;  // measured slower than unsplit on B200 (fix-up tail); option "splitk"
+  int choose_splits(int M, int N, int K, int bn) const {
+    if (!use_splitk) return 1;
+    const int tiles = cdiv(N, bn) * cdiv(M, TC_BM);
+    const int kb = K / TC_BK;
+    int S = 1;
+    while (S * 2 <= 8 && tiles * S * 2 <= num_sms && kb / (S * 2) >= 2) S *= 2;
+    while (S > 1 && (size_t)S * cdiv(M, TC_BM) * TC_BM * N * sizeof(float) > sk_ws_bytes) S /= 2;
+    if (tiles > sk_max_tiles) S = 1;
+    return S;
+  }
+
   template <int BN, int ST, class Epi>
   void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
     if constexpr (BF16) {
@@ -638,14 +663,20 @@ struct Engine : EngineBase {
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN);
       const int tiles = cdiv(N, BN) * cdiv(M, TC_BM);  // M: count, or upper bound with M_dev
-      launch(kern, std::min(tiles, num_sms), TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi);
+      SplitK sk{1, sk_ws, sk_counters};
+      if constexpr (!Epi::kRowWise) sk.splits = choose_splits(M, N, K, BN);
+      launch(kern, std::min(tiles * sk.splits, num_sms), TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi, sk);
     }
   }
 
+  // widest N tile that still fills ~0.6 of the SMs (large-M encoder / Stage-II
+  // GEMMs -> 256, Stage-I GEMMs with few row tiles -> 128 or 64)
   int choose_bn(int M, int N) const {
     if (M <= 128) return 64;
-    if (N >= 4096) return 256;
-    return 128;
+    const int mt = cdiv(M, TC_BM);
+    for (int bn : {256, 128})
+      if (mt * cdiv(N, bn) * 10 >= num_sms * 6) return bn;
+    return 64;
   }
 
   // C[M,N] = A[M,K] . W[N,K]^T with a fused epilogue
@@ -679,6 +710,19 @@ struct Engine : EngineBase {
                  float* y32 = nullptr, const int* M_dev = nullptr) {
     if (M <= 0) return;
     Scope sc(this, K_OTHER, (double)M * d * (4 + sizeof(T)), 8.0 * M * d);
+    if (d % 128 == 0 && d <= 1024) {
+      const int nv = d / 128;
+#define HRT_LNV(N) launch(layernorm_vec_kernel<T, N>, cdiv(M, 8), 256, 0, x, M_dev, M, d, g, b, y, out_row, y32)
+      if (nv == 1) HRT_LNV(1);
+      else if (nv == 2) HRT_LNV(2);
+      else if (nv == 4) HRT_LNV(4);
+      else if (nv == 8) HRT_LNV(8);
+      else goto scalar_ln;
+#undef HRT_LNV
+      check_launch();
+      return;
+    }
+  scalar_ln:
     const int npl = cdiv(d, 32);
 #define HRT_LN(N) ln_launch<N>(x, M_dev, M, g, b, y, out_row, y32)
     if (npl <= 1) HRT_LN(1);
@@ -802,6 +846,9 @@ struct Engine : EngineBase {
       if (kt == 1) {
         VocabEpi<1> epi{parts, norm_allowed, bn};
         launch_vocab(y, y_cap, R, epi, bn, M_dev);
+      } else if (kt <= 5) {
+        VocabEpi<5> epi{parts, norm_allowed, bn};
+        launch_vocab(y, y_cap, R, epi, bn, M_dev);
       } else {
         VocabEpi<KTOP_MAX> epi{parts, norm_allowed, bn};
         launch_vocab(y, y_cap, R, epi, bn, M_dev);
@@ -832,6 +879,8 @@ struct Engine : EngineBase {
         dim3 grid(rn, parts.ntiles);
         if (kt == 1)
           launch(rowstats_from_logits_kernel<1>, grid, 32, 0, logits_buf, V, V, nullptr, sub, 256, norm_allowed);
+        else if (kt <= 5)
+          launch(rowstats_from_logits_kernel<5>, grid, 32, 0, logits_buf, V, V, nullptr, sub, 256, norm_allowed);
         else
           launch(rowstats_from_logits_kernel<KTOP_MAX>, grid, 32, 0, logits_buf, V, V, nullptr, sub, 256,
                  norm_allowed);
@@ -1236,15 +1285,22 @@ struct Engine : EngineBase {
       decoder_step(R, t, t * k, cap_max, s_feed, s_hist, s_rowseq, src_off, src_len, max_src, ctl, false, s_hist2);
       {
         Tag _tg(this, "s1.vocab");
-        vocab_parts(s1.y, R_max, R, s1.parts, KTOP_MAX, 0, s1.logits, Rd);
+        if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, beam + 1, 0, s1.logits, Rd);
       }
       Tag _tg(this, "s1.select");
       Scope sc(this, K_OTHER, 0, 0);
-      launch(rowstat_kernel<KTOP_MAX>, cdiv(R, 4), 128, 0, s1.parts, R, beam + 1, s1.rowstat, Rd);
-      check_launch();
-      const int S = cdiv(R, beam);
-      launch(beam_select_kernel<T>, cdiv(S, 4), 128, 0, s1.rowstat, bs, S, t, k, ctl);
-      check_launch();
+      if (!(s1_skip & 16)) {
+        if (beam + 1 <= 5)
+          launch(rowstat_kernel<5>, cdiv(R, 4), 128, 0, s1.parts, R, beam + 1, s1.rowstat, Rd);
+        else
+          launch(rowstat_kernel<KTOP_MAX>, cdiv(R, 4), 128, 0, s1.parts, R, beam + 1, s1.rowstat, Rd);
+        check_launch();
+      }
+      if (!(s1_skip & 32)) {
+        const int S = cdiv(R, beam);
+        launch(beam_select_kernel<T>, S, 32 * BEAM_MAX, 0, s1.rowstat, bs, S, t, k, ctl);
+        check_launch();
+      }
     }
   }
 
@@ -1288,6 +1344,8 @@ struct Engine : EngineBase {
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
+    else if (name == "splitk")
+      use_splitk = value != 0;
     else if (name == "stage1_skip") {
       s1_skip = value;
       for (auto& kv : loop_graphs) {

@@ -19,46 +19,66 @@ constexpr int KTOP_MAX = 8;  // top-k width kept per vocab row (beam <= 7)
 // ---------------------------------------------------------------------------
 template <typename T, int NPL>
 __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restrict__ pos, int pos_const,
-                                const int* __restrict__ pos_dev, const int* __restrict__ M_dev, int M, int d, float scale, const T* __restrict__ E,
-                                const float* __restrict__ pe, const float* __restrict__ g,
-                                const float* __restrict__ b, float* __restrict__ x, T* __restrict__ y) {
+                                const int* __restrict__ pos_dev, const int* __restrict__ M_dev, int M, int d,
+                                float scale, const T* __restrict__ E, const float* __restrict__ pe,
+                                const float* __restrict__ g, const float* __restrict__ b, float* __restrict__ x,
+                                T* __restrict__ y);
+
+// ---------------------------------------------------------------------------
+// Vectorised LayerNorm for d % 128 == 0: each lane owns NV float4 chunks of
+// the row (16-byte loads, NV independent loads in flight per lane).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void store4v(T* p, float4 v);
+template <>
+__device__ __forceinline__ void store4v<float>(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+template <>
+__device__ __forceinline__ void store4v<bf16>(bf16* p, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+template <typename T, int NV>
+__global__ void layernorm_vec_kernel(const float* __restrict__ x, const int* __restrict__ M_dev, int M, int d,
+                                     const float* __restrict__ g, const float* __restrict__ b, T* __restrict__ y,
+                                     const int* __restrict__ out_row, float* __restrict__ y32) {
   pdl_enter();
   if (M_dev) M = *M_dev;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  const int id = ids[row];
-  const int p = pos ? pos[row] : (pos_dev ? *pos_dev : pos_const);
-  float v[NPL];
+  const int orow = out_row ? out_row[row] : row;
+  if (orow < 0) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
+  float4 v[NV];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int j = lane + 32 * i;
-    if (j < d) {
-      v[i] = __fadd_rn(__fmul_rn(to_f(E[(size_t)id * d + j]), scale), pe[(size_t)p * d + j]);
-      s += v[i];
-    } else {
-      v[i] = 0.f;
-    }
-  }
+  for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   const float mean = warp_sum(s) / d;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int j = lane + 32 * i;
-    if (j < d) {
-      const float c = v[i] - mean;
-      q += c * c;
-    }
+  for (int i = 0; i < NV; ++i) {
+    const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+    q += (a * a + bb * bb) + (c * c + e * e);
   }
   const float inv = 1.0f / sqrtf(warp_sum(q) / d + 1e-5f);
 #pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int j = lane + 32 * i;
-    if (j < d) {
-      x[(size_t)row * d + j] = v[i];
-      y[(size_t)row * d + j] = from_f<T>((v[i] - mean) * inv * g[j] + b[j]);
-    }
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = (lane + 32 * i) * 4;
+    const float4 gg = *reinterpret_cast<const float4*>(g + c4);
+    const float4 bv = *reinterpret_cast<const float4*>(b + c4);
+    float4 o;
+    o.x = (v[i].x - mean) * inv * gg.x + bv.x;
+    o.y = (v[i].y - mean) * inv * gg.y + bv.y;
+    o.z = (v[i].z - mean) * inv * gg.z + bv.z;
+    o.w = (v[i].w - mean) * inv * gg.w + bv.w;
+    store4v<T>(y + (size_t)orow * d + c4, o);
+    if (y32) store4v<float>(y32 + (size_t)orow * d + c4, o);
   }
 }
 
@@ -659,19 +679,20 @@ struct TileAcc {
       id[i] = 0x7fffffff;
     }
   }
+  // bubble (v, c) into the sorted list with static indices only, so the
+  // list stays in registers (a dynamic insert position spills it to local memory)
   __device__ __forceinline__ void insert(float v, int c) {
     if (!better(v, c, val[KT - 1], id[KT - 1])) return;
-    int p = KT - 1;
 #pragma unroll
-    for (int i = KT - 1; i > 0; --i) {
-      if (p == i && better(v, c, val[i - 1], id[i - 1])) {
-        val[i] = val[i - 1];
-        id[i] = id[i - 1];
-        p = i - 1;
-      }
+    for (int i = 0; i < KT; ++i) {
+      const bool b = better(v, c, val[i], id[i]);
+      const float tv = b ? val[i] : v;
+      const int tc = b ? id[i] : c;
+      val[i] = b ? v : val[i];
+      id[i] = b ? c : id[i];
+      v = tv;
+      c = tc;
     }
-    val[p] = v;
-    id[p] = c;
   }
   // fold a new normaliser max in, rescaling the running sum
   __device__ __forceinline__ void rebase(float cm) {
@@ -916,11 +937,61 @@ struct GreedyState {
   int cap;
 };
 
-// Embedding + LayerNorm of one row by one warp (generic d <= 1024).
+// Embedding + LayerNorm of one row by one warp (generic d <= 1024):
+//   x = E[tok] * sqrt(d) + PE[pos] (fp32, unfused mul/add as the reference),
+//   y = LN1(x).  d % 256 == 0 takes the vectorised path (8 elements / lane / chunk).
+template <typename T, int NC>
+__device__ __forceinline__ void warp_embed_ln_vec(const T* __restrict__ E, const float* __restrict__ pe,
+                                                  const float* __restrict__ g, const float* __restrict__ b,
+                                                  float scale, int d, int tok, int pos, float* __restrict__ x,
+                                                  T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  float v[NC][8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = (lane + 32 * c) * 8;
+    float e8[8];
+    load8(E + (size_t)tok * d + j, e8);
+    const float4 p0 = *reinterpret_cast<const float4*>(pe + (size_t)pos * d + j);
+    const float4 p1 = *reinterpret_cast<const float4*>(pe + (size_t)pos * d + j + 4);
+    const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[c][e] = __fadd_rn(__fmul_rn(e8[e], scale), pp[e]);
+      s += v[c][e];
+    }
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float a = v[c][e] - mean;
+      q += a * a;
+    }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / d + 1e-5f);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = (lane + 32 * c) * 8;
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = (v[c][e] - mean) * inv * g[j + e] + b[j + e];
+    *reinterpret_cast<float4*>(x + j) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+    *reinterpret_cast<float4*>(x + j + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+    store4v<T>(y + j, make_float4(o[0], o[1], o[2], o[3]));
+    store4v<T>(y + j + 4, make_float4(o[4], o[5], o[6], o[7]));
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void warp_embed_ln(const T* __restrict__ E, const float* __restrict__ pe,
                                               const float* __restrict__ g, const float* __restrict__ b, float scale,
                                               int d, int tok, int pos, float* __restrict__ x, T* __restrict__ y) {
+  if (d == 512) return warp_embed_ln_vec<T, 2>(E, pe, g, b, scale, d, tok, pos, x, y);
+  if (d == 1024) return warp_embed_ln_vec<T, 4>(E, pe, g, b, scale, d, tok, pos, x, y);
+  if (d == 256) return warp_embed_ln_vec<T, 1>(E, pe, g, b, scale, d, tok, pos, x, y);
   const int lane = threadIdx.x & 31;
   float v[32];
   float s = 0.f;
@@ -952,6 +1023,20 @@ __device__ __forceinline__ void warp_embed_ln(const T* __restrict__ E, const flo
       y[j] = from_f<T>((v[i] - mean) * inv * g[j] + b[j]);
     }
   }
+}
+
+template <typename T, int NPL>
+__global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restrict__ pos, int pos_const,
+                                const int* __restrict__ pos_dev, const int* __restrict__ M_dev, int M, int d,
+                                float scale, const T* __restrict__ E, const float* __restrict__ pe,
+                                const float* __restrict__ g, const float* __restrict__ b, float* __restrict__ x,
+                                T* __restrict__ y) {
+  pdl_enter();
+  if (M_dev) M = *M_dev;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const int p = pos ? pos[row] : (pos_dev ? *pos_dev : pos_const);
+  warp_embed_ln<T>(E, pe, g, b, scale, d, ids[row], p, x + (size_t)row * d, y + (size_t)row * d);
 }
 
 template <typename T, int KT>
@@ -1113,11 +1198,20 @@ __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __r
       best_cmlm = cmlm;
     }
   }
+  const int dst = out.out_index ? out.out_index[s] : s;
+  if (best < 0) {  // no finished hypothesis reached Stage II (cannot happen with a step cap)
+    if (lane == 0) {
+      out.lens[dst] = 0;
+      out.scores[(size_t)dst * 3 + 0] = out.scores[(size_t)dst * 3 + 1] = out.scores[(size_t)dst * 3 + 2] = 0.0;
+      out.calls[dst] = cands.steps[s] + 1;
+      out.forced[dst] = 0;
+    }
+    return;
+  }
   const int c = best;
   const int T = qlen[c];
   const int o = off[c];
   const int mo = mrow_off[c];
-  const int dst = out.out_index ? out.out_index[s] : s;
   // first EOS in the filled sequence (warp scan over positions)
   int first_eos = T;
   for (int j0 = 0; j0 < T; j0 += 32) {
@@ -1220,28 +1314,31 @@ __global__ void beam_init_kernel(BeamState st, int S, int bos) {
   }
 }
 
+// grid = sentences (upper bound), block = 32 * BEAM_MAX threads: warp 0 runs
+// the selection, then warp j embeds row j of the sentence for the next step.
 template <typename T>
-__global__ void __launch_bounds__(128) beam_select_kernel(const RowStat* __restrict__ rs, BeamState st, int S, int t,
-                                                          int k, StepCtl* ctl) {
+__global__ void __launch_bounds__(32 * BEAM_MAX) beam_select_kernel(const RowStat* __restrict__ rs, BeamState st,
+                                                                   int S, int t, int k, StepCtl* ctl) {
   pdl_enter();
-  __shared__ double cs[4][BEAM_MAXC];
-  __shared__ int ct[4][BEAM_MAXC], cp[4][BEAM_MAXC], cg[4][BEAM_MAXC], ord[4][BEAM_MAXC];
-  __shared__ int nl_s[4], brk_s[4], ntok[4][BEAM_MAX], npar[4][BEAM_MAX], ncopy[4], copy_slot[4][BEAM_MAXC],
-      copy_src[4][BEAM_MAXC];
+  __shared__ double cs[1][BEAM_MAXC];
+  __shared__ int ct[1][BEAM_MAXC], cp[1][BEAM_MAXC], cg[1][BEAM_MAXC], ord[1][BEAM_MAXC];
+  __shared__ int nl_s[1], brk_s[1], ntok[1][BEAM_MAX], npar[1][BEAM_MAX], ncopy[1], copy_slot[1][BEAM_MAXC],
+      copy_src[1][BEAM_MAXC];
   const int beam = st.beam;
   if (ctl) {
     S = ctl->R / beam;
     t = ctl->t;
     k = ctl->k;
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * (blockDim.x >> 5) + w;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = 0;
+  const int s = blockIdx.x;
   if (s >= S) return;
   const int r0 = s * beam;
   const int cur = t & 1, nxt = cur ^ 1;
   const int cap = st.cap;
   const int F = st.bnat + 2;
-  if (!st.done[s]) {
+  if (wid == 0 && !st.done[s]) {
     const int L = st.live_n[s];
     const bool last = (t == st.caps[s] - 1);
     const int nt = last ? 1 : beam + 1;
@@ -1398,15 +1495,13 @@ __global__ void __launch_bounds__(128) beam_select_kernel(const RowStat* __restr
       }
     }
   }
-  __syncwarp();
-  // next step's embedding for all rows of the sentence (finished ones feed stale tokens)
-  if (st.x != nullptr) {
-    for (int j = 0; j < beam; ++j) {
-      const int r = r0 + j;
-      const int tok = st.feed[r];
-      warp_embed_ln<T>(static_cast<const T*>(st.E), st.pe, st.ln_g, st.ln_b, st.scale, st.d, tok, (t + 1) * k,
-                       st.x + (size_t)r * st.d, static_cast<T*>(st.y) + (size_t)r * st.d);
-    }
+  __syncthreads();
+  // next step's embedding, one warp per row (finished rows feed stale tokens)
+  if (st.x != nullptr && wid < beam) {
+    const int r = r0 + wid;
+    const int tok = st.feed[r];
+    warp_embed_ln<T>(static_cast<const T*>(st.E), st.pe, st.ln_g, st.ln_b, st.scale, st.d, tok, (t + 1) * k,
+                     st.x + (size_t)r * st.d, static_cast<T*>(st.y) + (size_t)r * st.d);
   }
 }
 

@@ -49,10 +49,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //    (N % 4 == 0 is required).
 //  row-wise (Epi::kRowWise == true): State; begin(st,row,n0);
 //    chunk(st,row,col0,const float* v,int n); end(st,row,n0) per thread-row.
+// Split-K: splits > 1 partitions the K blocks of every tile into slices,
+// each slice an independent work unit; ws holds splits x Mpad x N fp32
+// partials and counters one arrival counter per tile (zero between launches).
+struct SplitK {
+  int splits;
+  float* ws;
+  int* counters;
+};
+
 template <int BN, int STAGES, class Epi>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, const int* __restrict__ M_dev, Epi epi) {
+                   int K, const int* __restrict__ M_dev, Epi epi, SplitK sk) {
   using L = TcSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -91,7 +100,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (M_dev != nullptr) M = *M_dev;
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  // work unit = (tile, k-slice); sk.splits > 1 only for element-wise epilogues
+  const int S = sk.splits;
+  const int num_units = m_tiles * n_tiles * S;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -99,9 +110,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol_w = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int tile = u / S, ks = u - tile * S;
         const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -121,13 +134,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+        const int ks = u % S;
+        const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
             tc_mma_f16(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
-                       (kb | k) != 0);
+                       ((kb - kb0) | k) != 0);
           tc_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -151,7 +166,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * 33);
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      const int tile = u / S, ks = u - tile * S;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
@@ -175,6 +192,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (live) epi.end(st, row, n0);
       } else {
+        const int Mpad = m_tiles * TC_BM;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
@@ -189,10 +207,56 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const float* s = stg + (i * 4 + (lane >> 3)) * 33 + (lane & 7) * 4;
             vals[i] = make_float4(s[0], s[1], s[2], s[3]);
           }
-          // rows rbase + (lane >> 3) + 4 i; all global loads of the group are
-          // issued before any store (memory-level parallelism)
-          if (col < N) epi.apply8(rbase + (lane >> 3), col, vals, M);
+          if (S == 1) {
+            // rows rbase + (lane >> 3) + 4 i; all global loads of the group are
+            // issued before any store (memory-level parallelism)
+            if (col < N) epi.apply8(rbase + (lane >> 3), col, vals, M);
+          } else if (col < N) {
+            // split-K: this slice's fp32 partial tile
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int row = rbase + (lane >> 3) + 4 * i;
+              *reinterpret_cast<float4*>(sk.ws + ((size_t)ks * Mpad + row) * N + col) = vals[i];
+            }
+          }
           __syncwarp();
+        }
+        if (S > 1) {
+          // deterministic split-K fix-up: the last slice to finish sums all
+          // partials in slice order and applies the real epilogue
+          __threadfence();
+          asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32));
+          if (ew == 0 && lane == 0) {
+            const int old = atomicAdd(sk.counters + tile, 1);
+            *last_flag = (old == S - 1);
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32));
+          if (*last_flag) {
+            __threadfence();
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+              const int col = n0 + c + (lane & 7) * 4;
+              if (col >= N) continue;
+              float4 vals[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) vals[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+              for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int row = rbase + (lane >> 3) + 4 * i;
+                  const float4 p = __ldcg(reinterpret_cast<const float4*>(sk.ws + ((size_t)s2 * Mpad + row) * N + col));
+                  vals[i].x += p.x;
+                  vals[i].y += p.y;
+                  vals[i].z += p.z;
+                  vals[i].w += p.w;
+                }
+              }
+              epi.apply8(rbase + (lane >> 3), col, vals, M);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32));
+            if (ew == 0 && lane == 0) sk.counters[tile] = 0;  // re-arm for the next launch / graph replay
+          }
         }
       }
       tc_fence_before();

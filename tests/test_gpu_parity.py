@@ -293,3 +293,19 @@ def test_fused_beam_bf16_graph_equals_eager(hrt, golden):
         b = eng.translate_batch(srcs, 2, b_at, b_nat, max_steps=caps)
         for x, y in zip(a, b):
             assert x.tokens == y.tokens and x.score == y.score and x.decoder_calls == y.decoder_calls
+
+
+def test_splitk_equals_unsplit_and_is_deterministic(hrt, golden):
+    """Split-K GEMMs (deterministic last-arriver reduction) change only fp32
+    summation order: tokens match the unsplit engine and repeat bit-exactly."""
+    g = golden("dh64")
+    eng = hrt.Engine(_model(hrt, g), dtype="bfloat16", max_sentences=8, max_beam=4)
+    srcs = g["sources"]
+    runs = []
+    for sk in (1, 1, 0):
+        eng.set_option("splitk", sk)
+        runs.append(eng.translate_batch(srcs, 2, 4, 2))
+    for a, b in zip(runs[0], runs[1]):
+        assert a.tokens == b.tokens and a.score == b.score
+    agree = sum(x.tokens == y.tokens for x, y in zip(runs[0], runs[2]))
+    assert agree >= len(srcs) - 1

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--uniform-cap", type=int, default=0)
     a = ap.parse_args()
     import torch
 
@@ -30,6 +31,8 @@ def main():
     spec = W.CONFIGS[a.config]
     srcs = W.make_sources(a.batch, spec["seed"] + 1000, spec["lengths"])
     caps = W.stage1_caps(srcs, spec["k"])
+    if a.uniform_cap:
+        caps = [a.uniform_cap] * len(caps)
     eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]),
                      dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", max_sentences=a.batch,
                      max_beam=spec["beam"])
@@ -38,11 +41,11 @@ def main():
     ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
     lens = [len(s) for s in srcs]
     for _ in range(2):
-        out = eng.translate_arrays(ids, lens, k=spec["k"], max_steps=caps)
+        out = eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     for _ in range(a.repeat):
-        out = eng.translate_arrays(ids, lens, k=spec["k"], max_steps=caps)
+        out = eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     eng.synchronize()
     torch.cuda.profiler.stop()
     print("words", int(out["lens"].sum()), "launches", eng.stats()["kernel_launches"])

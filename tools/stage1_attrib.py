@@ -1,23 +1,36 @@
 """Graph-mode Stage-I time with kernel groups dropped (debug attribution)."""
-import os, sys
+import argparse, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2212_01543_b200 as hrt
 from paper_2212_01543_b200 import workload as W
 
-spec = W.CONFIGS["c2"]
-eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=1024, max_beam=1)
-for B in (1, 64, 1024):
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--batches", default="1,64,1024")
+ap.add_argument("--steps", type=int, default=30)
+a = ap.parse_args()
+spec = W.CONFIGS[a.config]
+Bs = [int(x) for x in a.batches.split(",")]
+eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=max(Bs),
+                 max_beam=spec["beam"])
+names = ((0, "full"), (1, "-LN"), (4, "-gemm"), (8, "-vocab"), (16, "-select/rowstat"),
+         (32, "-embed/beam_sel"), (2, "-attn"))
+for B in Bs:
     srcs = W.make_sources(B, 1001, spec["lengths"])
-    caps = [30] * B
+    caps = [a.steps] * B
     ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
     lens = [len(s) for s in srcs]
-    for mask, name in ((0, "full"), (1, "-LN"), (2, "-attn"), (4, "-gemm"), (8, "-vocab"), (16, "-select"),
-                       (32, "-embed"), (63, "-all")):
+    for mask, name in names:
         eng.set_option("stage1_skip", mask)
         t = []
-        for _ in range(4):
-            eng.translate_arrays(ids, lens, k=2, max_steps=caps)
-            t.append(eng.phase_times()["stage1"])
-        print(f"B={B:5d} {name:8s} stage1 {min(t[1:]):8.3f} ms  per step {1000*min(t[1:])/30:7.1f} us", flush=True)
+        try:
+            for _ in range(4):
+                eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
+                t.append(eng.phase_times()["stage1"])
+        except Exception as ex:  # skipped kernels can leave garbage state
+            print(f"B={B:5d} {name:16s} failed: {type(ex).__name__}", flush=True)
+            break
+        print(f"B={B:5d} {name:16s} stage1 {min(t[1:]):8.3f} ms  per step {1000*min(t[1:])/a.steps:7.1f} us",
+              flush=True)
 eng.set_option("stage1_skip", 0)

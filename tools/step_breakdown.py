@@ -20,13 +20,14 @@ def main():
     if a.uniform_cap:
         caps = [a.uniform_cap] * len(caps)
     eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]),
-                     dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", max_sentences=a.batch, max_beam=1)
+                     dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", max_sentences=a.batch,
+                     max_beam=spec["beam"])
     ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
     lens = [len(s) for s in srcs]
     for _ in range(2):
-        eng.translate_arrays(ids, lens, k=spec["k"], max_steps=caps)
+        eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     eng.timing_enable("all", True)
-    eng.translate_arrays(ids, lens, k=spec["k"], max_steps=caps)
+    eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     rep = eng.timing_report()
     eng.timing_enable("all", False)
     tot = sum(v[0] for v in rep.values())
@@ -34,7 +35,7 @@ def main():
     print(f"batch {a.batch}: {tot:.3f} ms in timed launches, Stage-I steps {steps}")
     for k, (ms, n) in sorted(rep.items(), key=lambda x: -x[1][0]):
         print(f"  {k:18s} {ms:8.3f} ms {n:6d} launches {1000*ms/n:8.2f} us/launch")
-    eng.translate_arrays(ids, lens, k=spec["k"], max_steps=caps)
+    eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     print("graph-mode phases (ms):", eng.phase_times())
 
 

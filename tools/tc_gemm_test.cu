@@ -49,7 +49,7 @@ bool run(int M, int N, int K) {
   int tiles = ((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
   dim3 grid(tiles < nsm ? tiles : nsm);
   StoreEpi epi{dC, N};
-  kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi, SplitK{1, nullptr, nullptr});
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<float> hC((size_t)M * N);
@@ -72,10 +72,10 @@ bool run(int M, int N, int K) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int w = 0; w < 3; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  for (int w = 0; w < 3; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi, SplitK{1, nullptr, nullptr});
   cudaEventRecord(e0);
   const int iters = 20;
-  for (int w = 0; w < iters; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi);
+  for (int w = 0; w < iters; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi, SplitK{1, nullptr, nullptr});
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms;
