@@ -494,7 +494,7 @@ struct Engine : EngineBase {
   // partials per row for the selection merge, one tile per CTA at small R)
   int vocab_bn(int rows) const { return V >= 4096 ? 256 : choose_bn(rows, V); }
   // upper bound on vocab tiles per row for any row count (partials sizing)
-  int nt_bound() const { return (BF16 && V < 4096) ? cdiv(V, 64) : cdiv(V, 256); }
+  int nt_bound() const { return (BF16 && V < 4096) ? cdiv(V, 32) : cdiv(V, 128); }
 
   void carve(int phase, Plan& p, char* base) {
     if (phase == 0) {
@@ -841,16 +841,16 @@ struct Engine : EngineBase {
     if (R <= 0) return;
     if constexpr (BF16) {
       const int bn = vocab_bn(R);
-      parts.ntiles = cdiv(V, bn);
+      parts.ntiles = cdiv(V, bn / 2);  // one partial per epilogue column half
       Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
       if (kt == 1) {
-        VocabEpi<1> epi{parts, norm_allowed, bn};
+        VocabEpi<1> epi{parts, norm_allowed, bn / 2};
         launch_vocab(y, y_cap, R, epi, bn, M_dev);
       } else if (kt <= 5) {
-        VocabEpi<5> epi{parts, norm_allowed, bn};
+        VocabEpi<5> epi{parts, norm_allowed, bn / 2};
         launch_vocab(y, y_cap, R, epi, bn, M_dev);
       } else {
-        VocabEpi<KTOP_MAX> epi{parts, norm_allowed, bn};
+        VocabEpi<KTOP_MAX> epi{parts, norm_allowed, bn / 2};
         launch_vocab(y, y_cap, R, epi, bn, M_dev);
       }
       check_launch();

@@ -7,7 +7,8 @@
 //   warp 0        TMA producer (one elected lane), STAGES-deep smem ring
 //   warp 1        TMEM allocator + MMA issuer (one elected lane); two TMEM
 //                 accumulators so tile i+1's MMAs overlap tile i's epilogue
-//   warps 2..2+E  epilogue. Element-wise epilogues (bias / ReLU / residual /
+//   warps 2..9    epilogue, two warps per TMEM lane quarter (column halves).
+//                 Element-wise epilogues (bias / ReLU / residual /
 //                 store) transpose each 32x32 accumulator chunk through a
 //                 per-warp smem buffer so global traffic is coalesced 128 B
 //                 rows; row-wise epilogues (vocab softmax statistics) keep
@@ -20,7 +21,7 @@ namespace hrt {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
-constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half the tile columns
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
 template <int BN, int STAGES>
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ===== epilogue warps =====
     const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int cbeg = (ew / 4) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * 33);
     int it = 0;
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
@@ -180,9 +182,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int row = rbase + lane;
         typename Epi::State st;
         const bool live = row < M;
-        if (live) epi.begin(st, row, n0);
+        if (live) epi.begin(st, row, n0 + cbeg);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = cbeg; c < cend; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
           const int col0 = n0 + c;
@@ -190,11 +192,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           nvalid = nvalid > 32 ? 32 : nvalid;
           if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
         }
-        if (live) epi.end(st, row, n0);
+        if (live) epi.end(st, row, n0 + cbeg);
       } else {
         const int Mpad = m_tiles * TC_BM;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = cbeg; c < cend; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
 #pragma unroll
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (*last_flag) {
             __threadfence();
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = cbeg; c < cend; c += 32) {
               const int col = n0 + c + (lane & 7) * 4;
               if (col >= N) continue;
               float4 vals[8];
