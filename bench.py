@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--sweep", default="", help="comma list of extra batch sizes to report")
+    ap.add_argument("--streams", type=int, default=1, help="concurrent engines (CUDA streams) per GPU")
     return ap.parse_args()
 
 
@@ -225,71 +226,101 @@ def run_engine(args):
     spec, k, _, _ = workload(args, rank, 0)
     sh = spec["shape"]
     B = args.batch
+    S = max(1, min(args.streams, B))
     model = hrt.HRTModel.random(sh, spec["seed"])
     b_at = spec["beam"]
-    eng = hrt.Engine(model, dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", device=local,
-                     max_sentences=B, max_beam=b_at)
+    per = -(-B // S)
+    # S concurrent engines (one CUDA stream each) on this GPU: the batch is cut
+    # into S length buckets so latency-bound Stage-I tails overlap GEMM phases
+    engs = [hrt.Engine(model, dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", device=local,
+                       max_sentences=per, max_beam=b_at) for _ in range(S)]
+    eng = engs[0]
     del model
 
     batches = [workload(args, rank, s) for s in range(args.warmup + args.steps)]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-
-    def device_inputs(srcs):
-        ids = torch.tensor(np.concatenate([np.asarray(s, np.int32) for s in srcs]), dtype=torch.int32,
-                           device="cuda")
-        lens = np.array([len(s) for s in srcs], np.int32)
-        return ids, lens
-
+    streams = [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local)) for e in engs]
+    stream = streams[0]
     L = sh.max_len
     dout = dict(tokens=torch.zeros((B, L), dtype=torch.int32, device="cuda"),
                 lens=torch.zeros(B, dtype=torch.int32, device="cuda"),
                 scores=torch.zeros((B, 3), dtype=torch.float64, device="cuda"),
                 calls=torch.zeros(B, dtype=torch.int32, device="cuda"),
                 forced=torch.zeros(B, dtype=torch.uint8, device="cuda"))
-    out_ptrs = [dout[n].data_ptr() for n in ("tokens", "lens", "scores", "calls", "forced")]
-
-    phases = []
-
-    def run_device(b):
-        _, _, srcs, caps = b
-        ids, lens = device_inputs(srcs)
-        torch.cuda.synchronize()
-        flush.zero_()
-        torch.cuda.synchronize()
-        e0, e1 = ev(), ev()
-        n0 = eng.stats()["kernel_launches"]
-        e0.record(stream)
-        eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps)
-        e1.record(stream)
-        e1.synchronize()
-        n1 = eng.stats()["kernel_launches"]
-        phases.append(eng.phase_times())
-        words = int(dout["lens"][: len(srcs)].sum().item())
-        return e0.elapsed_time(e1), words, n1 - n0
-
-    # pinned host buffers for e2e
     pin = lambda shape, dt: torch.zeros(shape, dtype={np.int32: torch.int32, np.float64: torch.float64,  # noqa
                                                       np.uint8: torch.uint8}[dt], pin_memory=True).numpy()
     hout = eng.alloc_outputs(B, pinned=pin)
+    phases = []
 
-    def run_host(b):
+    def chunks_of(caps, n):
+        order = np.argsort(-np.asarray(caps), kind="stable")
+        return [c for c in np.array_split(order, n) if len(c)]
+
+    def out_ptrs(start):
+        return [dout["tokens"][start:].data_ptr(), dout["lens"][start:].data_ptr(),
+                dout["scores"][start:].data_ptr(), dout["calls"][start:].data_ptr(),
+                dout["forced"][start:].data_ptr()]
+
+    def run_device(b, n_eng=None):
         _, _, srcs, caps = b
-        ids_h = pin((sum(len(s) for s in srcs),), np.int32)
-        ids_h[:] = np.concatenate([np.asarray(s, np.int32) for s in srcs])
-        lens = np.array([len(s) for s in srcs], np.int32)
+        n_eng = n_eng or S
+        parts, start = [], 0
+        for c in chunks_of(caps, n_eng):
+            ids = torch.tensor(np.concatenate([np.asarray(srcs[i], np.int32) for i in c]), dtype=torch.int32,
+                               device="cuda")
+            parts.append((ids, np.array([len(srcs[i]) for i in c], np.int32), [caps[i] for i in c], start))
+            start += len(c)
         torch.cuda.synchronize()
         flush.zero_()
         torch.cuda.synchronize()
-        e0, e1 = ev(), ev()
-        e0.record(stream)
-        eng.translate_arrays(ids_h, lens, k=k, b_at=b_at, max_steps=caps, out=hout)
-        e1.record(stream)
-        e1.synchronize()
-        h2d = ids_h.nbytes + lens.nbytes
-        d2h = sum(hout[n][: len(srcs)].nbytes for n in hout)
-        return e0.elapsed_time(e1), int(hout["lens"][: len(srcs)].sum()), h2d, d2h
+        e0 = ev()
+        e0.record(streams[0])
+        for st in streams[1:len(parts)]:
+            st.wait_event(e0)
+        n0 = sum(e.stats()["kernel_launches"] for e in engs)
+        ends = []
+        for e, st, (ids, lens, capc, st0) in zip(engs, streams, parts):
+            e.translate_device(ids.data_ptr(), lens, out_ptrs(st0), k=k, b_at=b_at, max_steps=capc)
+            e1 = ev()
+            e1.record(st)
+            ends.append(e1)
+        for e1 in ends:
+            e1.synchronize()
+        n1 = sum(e.stats()["kernel_launches"] for e in engs)
+        if len(parts) == 1:
+            phases.append(eng.phase_times())
+        words = int(dout["lens"][:start].sum().item())
+        return max(e0.elapsed_time(e1) for e1 in ends), words, n1 - n0
+
+    def run_host(b):
+        _, _, srcs, caps = b
+        parts, start = [], 0
+        for c in chunks_of(caps, S):
+            ids_h = pin((sum(len(srcs[i]) for i in c),), np.int32)
+            ids_h[:] = np.concatenate([np.asarray(srcs[i], np.int32) for i in c])
+            parts.append((ids_h, np.array([len(srcs[i]) for i in c], np.int32), [caps[i] for i in c], start))
+            start += len(c)
+        torch.cuda.synchronize()
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = ev()
+        e0.record(streams[0])
+        for st in streams[1:len(parts)]:
+            st.wait_event(e0)
+        ends = []
+        for e, st, (ids_h, lens, capc, st0) in zip(engs, streams, parts):
+            n = len(lens)
+            view = {key: arr[st0: st0 + n] for key, arr in hout.items()}
+            e.translate_arrays_async(ids_h, lens, k=k, b_at=b_at, max_steps=capc, out=view)
+            e1 = ev()
+            e1.record(st)
+            ends.append(e1)
+        for e1 in ends:
+            e1.synchronize()
+        h2d = sum(p[0].nbytes + p[1].nbytes for p in parts)
+        d2h = sum(hout[n][:start].nbytes for n in hout)
+        return max(e0.elapsed_time(e1) for e1 in ends), int(hout["lens"][:start].sum()), h2d, d2h
 
     # ---- warmup + timed (device-resident) ----
     for s in range(args.warmup):
@@ -309,7 +340,8 @@ def run_engine(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     tot_ms = sum(times)
-    phase_ms = {key: statistics.fmean(p[key] for p in phases) for key in ("encoder", "stage1", "stage2")}
+    phase_ms = ({key: statistics.fmean(p[key] for p in phases) for key in ("encoder", "stage1", "stage2")}
+                if phases else None)
     stage1_steps = statistics.fmean(max(b[3]) for b in batches[args.warmup:])
     # ---- e2e (host buffers) ----
     for s in range(min(2, args.warmup)):
@@ -321,17 +353,20 @@ def run_engine(args):
         e_words += w
         h2d, d2h = hb, db
     e_tot = sum(e_times)
-    # ---- roofline pass: GEMM class (tensor-bound at this batch) ----
+    # ---- roofline pass (engine 0 alone on one length bucket): GEMM class ----
+    rb = batches[args.warmup]
+    c0 = chunks_of(rb[3], S)[0]
+    one = (rb[0], rb[1], [rb[2][i] for i in c0], [rb[3][i] for i in c0])
     eng.timing_enable("gemm", True)
-    run_device(batches[args.warmup])
+    run_device(one, 1)
     g = eng.timing_read()
     eng.timing_enable("gemm", False)
     eng.timing_enable("vocab", True)
-    run_device(batches[args.warmup])
+    run_device(one, 1)
     vv = eng.timing_read()
     eng.timing_enable("vocab", False)
     eng.timing_enable("all", True)
-    ms_all, _, _ = run_device(batches[args.warmup])
+    ms_all, _, _ = run_device(one, 1)
     allk = eng.timing_read()
     eng.timing_enable("all", False)
 
@@ -377,19 +412,13 @@ def run_engine(args):
         for bs in [int(x) for x in args.sweep.split(",") if x]:
             if bs > B:
                 continue
-            _, _, srcs, caps = batches[args.warmup]
-            ids = torch.tensor(np.concatenate([np.asarray(s, np.int32) for s in srcs[:bs]]), device="cuda")
-            lens = np.array([len(s) for s in srcs[:bs]], np.int32)
+            rb = batches[args.warmup]
+            sub = (rb[0], rb[1], rb[2][:bs], rb[3][:bs])
+            n_eng = min(S, bs)
             for _ in range(2):
-                eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps[:bs])
-            torch.cuda.synchronize()
-            e0, e1 = ev(), ev()
-            e0.record(stream)
-            eng.translate_device(ids.data_ptr(), lens, out_ptrs, k=k, b_at=b_at, max_steps=caps[:bs])
-            e1.record(stream)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1)
-            sweep[str(bs)] = {"ms": ms, "target_words_per_s": int(dout["lens"][:bs].sum().item()) / (ms / 1e3)}
+                run_device(sub, n_eng)
+            ms, w, _ = run_device(sub, n_eng)
+            sweep[str(bs)] = {"ms": ms, "target_words_per_s": w / (ms / 1e3), "streams": n_eng}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -419,6 +448,8 @@ def run_engine(args):
                                f"V{sh.vocab_size}, batch {B} sentences/GPU/step, lengths {spec['lengths']}, "
                                f"Zipf(1.1) ids, random N(0,0.02) weights seed {spec['seed']}",
                    "batch_per_gpu": B, "k": k, "l2": "512 MiB flush between timed steps (outside events)",
+                   "streams": S, "scheduling": f"batch cut into {S} length buckets, one engine/CUDA stream each, "
+                                               "run concurrently (no inter-stream communication)",
                    "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e_tot / args.steps},

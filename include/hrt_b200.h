@@ -117,7 +117,9 @@ typedef struct hrt_translate_out {
  * lens and max_steps are HOST arrays (the schedule); max_steps NULL means the
  * reference default ceil(max_len / k) (decoding.py:202-203). When
  * io_on_device is 0, ids and every output pointer are host memory and the
- * copies are part of the call; when 1 they are device memory. */
+ * copies are part of the call; when 1 they are device memory; when 2 they are
+ * (pinned) host memory and the call returns without synchronising -- the
+ * caller uses hrt_synchronize (concurrent engines on one device). */
 hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t B, int32_t k,
                                int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
                                const hrt_translate_out* out, int32_t io_on_device);

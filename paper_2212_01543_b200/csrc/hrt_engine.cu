@@ -1578,7 +1578,8 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   meta_flush(cur);
   const int* src_ids = ids;
-  if (!on_device) {
+  const bool host_io = on_device != 1;
+  if (host_io) {
     CUDA_OK(cudaMemcpyAsync(d_ids_raw, ids, raw_off[B] * sizeof(int), cudaMemcpyHostToDevice, stream));
     src_ids = d_ids_raw;
   }
@@ -1658,11 +1659,11 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     check_launch();
   }
   Stage2Out so;
-  so.tokens = on_device ? out->tokens : o_tokens;
-  so.lens = on_device ? out->lens : o_lens;
-  so.scores = on_device ? out->scores : o_scores;
-  so.calls = on_device ? out->calls : o_calls;
-  so.forced = on_device ? out->forced : o_forced;
+  so.tokens = host_io ? o_tokens : out->tokens;
+  so.lens = host_io ? o_lens : out->lens;
+  so.scores = host_io ? o_scores : out->scores;
+  so.calls = host_io ? o_calls : out->calls;
+  so.forced = host_io ? o_forced : out->forced;
   so.out_index = d_perm;
   {
     Scope sc(this, K_OTHER, 0, 0);
@@ -1672,14 +1673,16 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   phase_mark(3);
   phase_valid = true;
-  if (!on_device) {
+  if (host_io) {
     CUDA_OK(cudaMemcpyAsync(out->tokens, o_tokens, (size_t)B * Lmax * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->lens, o_lens, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->scores, o_scores, B * 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->calls, o_calls, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->forced, o_forced, B, cudaMemcpyDeviceToHost, stream));
-    CUDA_OK(cudaStreamSynchronize(stream));
-    for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+    if (on_device == 0) {  // 2: host buffers, caller synchronises (concurrent engines)
+      CUDA_OK(cudaStreamSynchronize(stream));
+      for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+    }
   }
 }
 

@@ -160,6 +160,20 @@ class Engine:
                                                  int(b_nat), float(length_penalty), _ptr(ms), C.byref(o), 0))
         return out
 
+    def translate_arrays_async(self, ids, lens, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None, out=None):
+        """Like translate_arrays but returns once the work is enqueued; call
+        synchronize() before reading `out`. Keep ids/lens/out alive until then
+        (pinned host memory makes the copies truly asynchronous)."""
+        lens = _i32(lens)
+        ids = _i32(ids)
+        ms = None if max_steps is None else _i32(max_steps)
+        o = _lib.HrtTranslateOut(out["tokens"].ctypes.data, out["lens"].ctypes.data, out["scores"].ctypes.data,
+                                 out["calls"].ctypes.data, out["forced"].ctypes.data)
+        self._pending = (ids, lens, ms, o)
+        self._check(self.lib.hrt_translate_batch(self._h, ids.ctypes.data, _ptr(lens), int(lens.size), int(k),
+                                                 int(b_at), int(b_nat), float(length_penalty), _ptr(ms), C.byref(o), 2))
+        return out
+
     def translate_device(self, ids_dev_ptr, lens, out_ptrs, k=2, b_at=1, b_nat=1, length_penalty=0.6,
                          max_steps=None):
         """Device-resident ids/outputs (raw CUDA pointers); lens/max_steps on host."""
@@ -311,4 +325,51 @@ class CudaSession:
     def translate_batch(self, sources, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None):
         res = self.engine.translate_batch(sources, k, b_at, b_nat, length_penalty, max_steps)
         self.decoder_calls += sum(t.decoder_calls for t in res)
+        return res
+
+
+class EnginePool:
+    """Concurrent sub-batches on one device: `n` engines, one CUDA stream each.
+
+    `translate_batch` sorts the batch by Stage-I cap (source length), cuts it
+    into `n` contiguous length buckets and enqueues one fused call per engine
+    without waiting, so latency-bound Stage-I tail steps of one bucket overlap
+    with the GEMM-heavy phases of another. Results are returned in input
+    order and are identical to a single-engine call (sentences are independent).
+    """
+
+    def __init__(self, model, n=4, dtype="bfloat16", device=0, max_sentences=1024, max_beam=1, **kw):
+        per = -(-int(max_sentences) // int(n))
+        self.engines = [Engine(model, dtype=dtype, device=device, max_sentences=per, max_beam=max_beam, **kw)
+                        for _ in range(int(n))]
+        self.config = self.engines[0].config
+
+    def split(self, caps):
+        """Length buckets: indices sorted by cap (desc), cut into len(engines) runs."""
+        order = np.argsort(-np.asarray(caps), kind="stable")
+        return [c for c in np.array_split(order, len(self.engines)) if len(c)]
+
+    def translate_batch(self, sources, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None):
+        from .workload import stage1_caps
+
+        caps = list(max_steps) if max_steps is not None else stage1_caps(sources, k)
+        parts = self.split(caps)
+        outs = []
+        for eng, idx in zip(self.engines, parts):
+            srcs = [sources[i] for i in idx]
+            lens = np.array([len(s) for s in srcs], np.int32)
+            ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
+            out = eng.alloc_outputs(len(idx))
+            eng.translate_arrays_async(ids, lens, k, b_at, b_nat, length_penalty, [caps[i] for i in idx], out)
+            outs.append((idx, out, ids, lens))
+        from .decoding import Translation
+
+        res = [None] * len(sources)
+        for eng, (idx, out, _, _) in zip(self.engines, outs):
+            eng.synchronize()
+            for j, i in enumerate(idx):
+                n = int(out["lens"][j])
+                res[i] = Translation(tokens=out["tokens"][j, :n].tolist(), skip_at_score=float(out["scores"][j, 0]),
+                                     skip_cmlm_score=float(out["scores"][j, 1]), score=float(out["scores"][j, 2]),
+                                     decoder_calls=int(out["calls"][j]), forced=bool(out["forced"][j]))
         return res
