@@ -309,3 +309,28 @@ def test_splitk_equals_unsplit_and_is_deterministic(hrt, golden):
         assert a.tokens == b.tokens and a.score == b.score
     agree = sum(x.tokens == y.tokens for x, y in zip(runs[0], runs[2]))
     assert agree >= len(srcs) - 1
+
+
+def test_checkpoint_model_and_cli_translate(hrt, golden, tmp_path, capsys):
+    """HRTCKPT1 (written by the reference) -> engine: greedy and beam outputs
+    match the reference goldens; the CLI translate path prints them."""
+    import os
+
+    from paper_2212_01543_b200 import checkpoint as CK, cli
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    m = CK.load_model(os.path.join(here, "tiny_trained.ckpt"))
+    g = golden("tiny_trained")
+    sess = hrt.CudaSession(m, dtype=np.float32, max_sentences=len(g["sources"]), max_beam=4)
+    sel = [r for r in g["runs"] if r["k"] == 2 and r["b_at"] == 4 and r["b_nat"] == 4]
+    out = hrt.hrt_translate_batch(sess, [g["sources"][r["src"]] for r in sel], 2, 4, 4)
+    for tr, r in zip(out, sel):
+        _check_translation(tr, r["out"])
+    vocab = [ln.strip() for ln in open(os.path.join(here, "tiny_vocab.txt")) if ln.strip()]
+    src = tmp_path / "src.txt"
+    greedy = [r for r in g["runs"] if r["k"] == 2 and r["b_at"] == 1]
+    src.write_text("\n".join(" ".join(vocab[t] for t in g["sources"][r["src"]]) for r in greedy) + "\n")
+    cli.main(["translate", "--checkpoint", os.path.join(here, "tiny_trained.ckpt"), "--vocab",
+              os.path.join(here, "tiny_vocab.txt"), "--input", str(src), "--batch", "8"])
+    lines = capsys.readouterr().out.strip().split("\n")
+    assert lines == [" ".join(vocab[t] for t in r["out"]["tokens"]) for r in greedy]

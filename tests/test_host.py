@@ -149,3 +149,32 @@ def test_product_search_matches_golden_on_cpu(golden, name):
         for r in g["at_runs"]:
             tr = PD.at_translate(sess, g["sources"][r["src"]], beam=r["beam"])
             assert tr.tokens == r["out"]["tokens"] and abs(tr.score - r["out"]["score"]) < 1e-9
+
+
+def test_hrtckpt1_loader_reads_reference_checkpoint(golden, tmp_path):
+    """tests/golden/tiny_trained.ckpt was written by the reference's own
+    save_checkpoint (checkpoint.py:24-35); the loader must reproduce its
+    parameters exactly and round-trip through save_checkpoint."""
+    from paper_2212_01543_b200 import checkpoint as CK
+
+    g = golden("tiny_trained")
+    m = CK.load_model(os.path.join(REPO, "tests", "golden", "tiny_trained.ckpt"))
+    assert m.config.d_model == 16 and m.config.vocab_size == 15 and m.config.max_len == 6
+    for n, v in g["params"].items():
+        assert np.array_equal(m.params[n], np.asarray(v))
+    p = tmp_path / "rt.ckpt"
+    CK.save_checkpoint(m, p)
+    assert open(p, "rb").read() == open(os.path.join(REPO, "tests", "golden", "tiny_trained.ckpt"), "rb").read()
+    bad = tmp_path / "bad.ckpt"
+    bad.write_bytes(b"NOTACKPT" + b"\0" * 16)
+    with pytest.raises(CK.CheckpointError):
+        CK.load_model(bad)
+
+
+def test_cli_parser():
+    from paper_2212_01543_b200 import cli
+
+    a = cli.build_parser().parse_args(["translate", "--checkpoint", "m", "--vocab", "v", "--b-at", "4"])
+    assert a.b_at == 4 and a.k == 2 and a.input == "-"
+    a = cli.build_parser().parse_args(["bench", "--checkpoint", "m", "--vocab", "v", "--corpus", "c"])
+    assert a.runs == 5

@@ -198,7 +198,10 @@ def c1_case(n_sent=3):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["toy", "tiny_trained", "dh64", "c1"]
+    which = sys.argv[1:] or ["toy", "tiny_trained", "dh64", "c1", "ckpt"]
+    if "ckpt" in which:
+        which.remove("ckpt")
+        write_tiny_checkpoint()
     makers = dict(toy=toy_case, tiny_trained=tiny_trained_case, dh64=dh64_case, c1=c1_case)
     for name in which:
         data = makers[name]()
@@ -208,6 +211,23 @@ def main():
         with open(path, "w") as f:
             json.dump(data, f)
         print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+
+def write_tiny_checkpoint():
+    """The tiny_trained model saved by the reference's own save_checkpoint
+    (HRTCKPT1 fixture for the loader tests) plus its vocabulary file."""
+    from hrt.checkpoint import save_checkpoint
+    from hrt.data import Vocabulary, save_vocab
+
+    g = json.load(open(os.path.join(OUT, "tiny_trained.json")))
+    cfg = ModelConfig.from_dict(g["config"])
+    model = TransformerModel(cfg, seed=0)
+    for n, p in model.params.items():
+        p.data[...] = np.asarray(g["params"][n])
+    save_checkpoint(model, os.path.join(OUT, "tiny_trained.ckpt"))
+    save_vocab(Vocabulary.synthetic(cfg.vocab_size), os.path.join(OUT, "tiny_vocab.txt"))
+    print("wrote tiny_trained.ckpt / tiny_vocab.txt")
 
 
 if __name__ == "__main__":
