@@ -129,6 +129,9 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
 
 /* ---- measurement helpers ------------------------------------------------ */
+/* Debug: globaltimer stamps (ns) at each phase barrier of the first tail-megakernel
+ * step of the last call (option "mega_trace" must be on); up to 64 entries. */
+hrt_status hrt_debug_trace(hrt_engine* eng, int64_t* out, int32_t n);
 /* Kernel-class timing: when enabled, CUDA events bracket every launch of the
  * named class ("vocab", "gemm", "attn", "all") on the engine stream. */
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable);

@@ -20,7 +20,7 @@ HRT_DTYPE_F32, HRT_DTYPE_BF16 = 0, 1
 EXPORTED = (
     "hrt_create", "hrt_destroy", "hrt_param_count", "hrt_last_error", "hrt_get_stats", "hrt_stream",
     "hrt_synchronize", "hrt_encode", "hrt_start_cache", "hrt_step", "hrt_reorder", "hrt_parallel_logits",
-    "hrt_argmax_logprobs", "hrt_translate_batch", "hrt_set_option", "hrt_phase_times", "hrt_timing_enable",
+    "hrt_argmax_logprobs", "hrt_translate_batch", "hrt_set_option", "hrt_phase_times", "hrt_debug_trace", "hrt_timing_enable",
     "hrt_timing_report", "hrt_timing_read",
 )
 
@@ -77,6 +77,7 @@ def load(path: str | None = None):
                                  C.POINTER(HrtTranslateOut), i32], C.c_int),
         "hrt_set_option": ([vp, C.c_char_p, i32], C.c_int),
         "hrt_phase_times": ([vp, f32p], C.c_int),
+        "hrt_debug_trace": ([vp, C.POINTER(C.c_int64), i32], C.c_int),
         "hrt_timing_report": ([vp, C.c_char_p, i64], C.c_int),
         "hrt_timing_enable": ([vp, C.c_char_p, i32], C.c_int),
         "hrt_timing_read": ([vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),

@@ -25,6 +25,7 @@
 #include "gemm_epi.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "decode_mega.cuh"
 #include "tc_gemm.cuh"
 #include "tmap.h"
 
@@ -104,6 +105,7 @@ struct EngineBase {
                                const int32_t* seq, float* logits_out) = 0;
   virtual void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) = 0;
   virtual void set_option(const std::string& name, int value) = 0;
+  virtual void debug_trace(int64_t* out, int n) = 0;
   virtual void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
                          const int32_t* caps, const hrt_translate_out* out, int on_device) = 0;
 
@@ -209,6 +211,11 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
+  bool use_mega = false;  // option "mega": Stage-I tail (<= MG_RMAX live rows) in the cooperative megakernel (measured: no faster than the graph path)
+  float *mg_qkv = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr, *mg_vpart = nullptr, *mg_veos = nullptr;
+  unsigned* mg_bar = nullptr;
+  unsigned long long* mg_trace = nullptr;  // debug option "mega_trace"
+  bool mg_trace_on = false;
   // debug: drop kernel groups from the Stage-I step (timing attribution only;
   // results are meaningless when nonzero). 1 LN, 2 attention, 4 GEMMs,
   // 8 vocab, 16 select, 32 embed.
@@ -296,6 +303,12 @@ struct Engine : EngineBase {
     cudaFree(p_mem);
     cudaFree(sk_ws);
     cudaFree(sk_counters);
+    cudaFree(mg_qkv);
+    cudaFree(mg_ctx);
+    cudaFree(mg_hid);
+    cudaFree(mg_vpart);
+    cudaFree(mg_veos);
+    cudaFree(mg_bar);
     if (h_meta) cudaFreeHost(h_meta);
     for (auto& kv : loop_graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -614,6 +627,13 @@ struct Engine : EngineBase {
     }
     stats.arena_bytes = (int64_t)(arena_bytes + pbytes);
     if (BF16) {
+      CUDA_OK(cudaMalloc(&mg_qkv, (size_t)MG_RMAX * 3 * d * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_ctx, (size_t)MG_RMAX * d * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_hid, (size_t)MG_RMAX * ff * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_vpart, (size_t)MG_RMAX * num_sms * 4 * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_veos, MG_RMAX * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_bar, 2 * sizeof(unsigned)));
+      CUDA_OK(cudaMemset(mg_bar, 0, 2 * sizeof(unsigned)));
       CUDA_OK(cudaMalloc(&sk_ws, sk_ws_bytes));
       CUDA_OK(cudaMalloc(&sk_counters, sk_max_tiles * sizeof(int)));
       CUDA_OK(cudaMemset(sk_counters, 0, sk_max_tiles * sizeof(int)));
@@ -1304,6 +1324,76 @@ struct Engine : EngineBase {
     }
   }
 
+  bool mega_ok() const {
+    return BF16 && use_mega && dh == 64 && d % 256 == 0 && ff % 256 == 0 && Ld <= MG_MAX_LAYERS &&
+           timed_class == 0 && s1_skip == 0;
+  }
+  // Stage-I steps [t0, t1) in the cooperative tail megakernel (rows <= MG_RMAX)
+  void launch_mega(int t0, int t1, int k, int nrows, const GreedyState& gs) {
+    MegaParams mp{};
+    mp.d = d;
+    mp.ff = ff;
+    mp.H = H;
+    mp.V = V;
+    mp.Ld = Ld;
+    mp.cap = cap_max;
+    mp.k = k;
+    mp.rcap = R_max;
+    for (int i = 0; i < Ld; ++i) {
+      const DecW& w = dec[i];
+      mp.L[i] = MegaLayer{reinterpret_cast<const bf16*>(w.wqkv), reinterpret_cast<const bf16*>(w.wo),
+                          reinterpret_cast<const bf16*>(w.wqc),  reinterpret_cast<const bf16*>(w.woc),
+                          reinterpret_cast<const bf16*>(w.w1),   reinterpret_cast<const bf16*>(w.w2),
+                          w.bqkv, w.bo, w.bqc, w.boc, w.b1, w.b2, w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.ln3g, w.ln3b};
+    }
+    mp.lng = dec_lng;
+    mp.lnb = dec_lnb;
+    mp.E = reinterpret_cast<const bf16*>(E);
+    mp.pe = pe;
+    mp.scale = emb_scale;
+    mp.att_scale = att_scale;
+    mp.xkv = reinterpret_cast<const bf16*>(xkv);
+    mp.xstride = Ld * 2 * d;
+    mp.src_off = s_srcoff;
+    mp.src_len = s_srclen;
+    mp.kc = reinterpret_cast<bf16*>(s1.kc);
+    mp.vc = reinterpret_cast<bf16*>(s1.vc);
+    mp.x = s1.x;
+    mp.qkv = mg_qkv;
+    mp.ctx = mg_ctx;
+    mp.hid = mg_hid;
+    mp.vpart = mg_vpart;
+    mp.veos = mg_veos;
+    mp.st = gs;
+    mp.ctl = s_ctl;
+    mp.alive = s_alive;
+    mp.bar = mg_bar;
+    mp.t_begin = t0;
+    mp.t_end = t1;
+    mp.nrows = nrows;
+    mp.trace = mg_trace_on ? mg_trace : nullptr;
+    const size_t smem = ((size_t)MG_RMAX * std::max(d, ff) + (size_t)MG_WARPS * (cap_max + 4) +
+                         (size_t)MG_WARPS * MG_RMAX * 4) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_OK(cudaFuncSetAttribute(decode_mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    if (smem > 227 * 1024) throw HrtError(HRT_ERR_INVALID, "megakernel shared memory too large");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms);
+    cfg.blockDim = dim3(MG_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr2[1];
+    attr2[0].id = cudaLaunchAttributeCooperative;
+    attr2[0].val.cooperative = 1;
+    cfg.attrs = attr2;
+    cfg.numAttrs = 1;
+    Scope sc(this, K_OTHER, 0, 0);
+    CUDA_OK(cudaLaunchKernelEx(&cfg, decode_mega_kernel, mp));
+  }
+
   // Capture (once per row bucket and beam width) the Stage-I step as the body
   // of a conditional WHILE node. Every step-varying value lives in s_ctl.
   LoopGraph& loop_graph(int bucket, int beam, const GreedyState& gs, const BeamState& bs) {
@@ -1341,11 +1431,26 @@ struct Engine : EngineBase {
 
   void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) override;
 
+  void debug_trace(int64_t* out, int n) override {
+    if (!mg_trace) throw HrtError(HRT_ERR_INVALID, "enable option mega_trace first");
+    CUDA_OK(cudaStreamSynchronize(stream));
+    CUDA_OK(cudaMemcpy(out, mg_trace, std::min(n, 64) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
     else if (name == "splitk")
       use_splitk = value != 0;
+    else if (name == "mega")
+      use_mega = value != 0;
+    else if (name == "mega_trace") {
+      mg_trace_on = value != 0;
+      if (mg_trace_on && !mg_trace) {
+        CUDA_OK(cudaMalloc(&mg_trace, 64 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(mg_trace, 0, 64 * sizeof(unsigned long long)));
+      }
+    }
     else if (name == "stage1_skip") {
       s1_skip = value;
       for (auto& kv : loop_graphs) {
@@ -1618,21 +1723,34 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     Tag _tg(this, "s1.embed_ln");
     embed_ln(s_feed, nullptr, 0, alive.empty() ? 0 : alive[0], dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
   }
-  if (BF16 && use_graphs && timed_class == 0) {
-    // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
-    int bucket = 1;
-    while (bucket < B * beam) bucket <<= 1;
-    bucket = std::min(bucket, R_max);
-    LoopGraph& lg = loop_graph(bucket, beam, gs, bs);
-    CUDA_OK(cudaGraphLaunch(lg.exec, stream));
-    stats.kernel_launches += (int64_t)lg.kernels * max_cap;
-  } else {
-    for (int t = 0; t < max_cap; ++t) {
-      const int R = alive[t];
-      if (R == 0) break;
-      stage1_step(R, t, k, beam, max_src, d_off, d_len, gs, bs, nullptr);
+  // steps whose live rows fit the tail megakernel run there (greedy, bf16)
+  int t_mega = max_cap;
+  if (greedy_mode && mega_ok()) {
+    t_mega = 0;
+    while (t_mega < max_cap && alive[t_mega] > MG_RMAX) ++t_mega;
+  }
+  if (t_mega > 0) {
+    if (t_mega < max_cap) {  // the regular loop stops where the megakernel takes over
+      StepCtl c{0, alive[0], 0, k, t_mega, B, 0, 0};
+      CUDA_OK(cudaMemcpyAsync(s_ctl, &c, sizeof(StepCtl), cudaMemcpyHostToDevice, stream));
+    }
+    if (BF16 && use_graphs && timed_class == 0) {
+      // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
+      int bucket = 1;
+      while (bucket < B * beam) bucket <<= 1;
+      bucket = std::min(bucket, R_max);
+      LoopGraph& lg = loop_graph(bucket, beam, gs, bs);
+      CUDA_OK(cudaGraphLaunch(lg.exec, stream));
+      stats.kernel_launches += (int64_t)lg.kernels * t_mega;
+    } else {
+      for (int t = 0; t < t_mega; ++t) {
+        const int R = alive[t];
+        if (R == 0) break;
+        stage1_step(R, t, k, beam, max_src, d_off, d_len, gs, bs, nullptr);
+      }
     }
   }
+  if (t_mega < max_cap) launch_mega(t_mega, max_cap, k, B, gs);
   phase_mark(2);
   // ---- phase 3: Stage II over the selected candidates ----
   Stage2Cands cands;
@@ -1801,6 +1919,10 @@ hrt_status hrt_phase_times(hrt_engine* eng, float* ms3) {
     CUDA_OK(cudaEventSynchronize(e->phase_ev[3]));
     for (int i = 0; i < 3; ++i) CUDA_OK(cudaEventElapsedTime(&ms3[i], e->phase_ev[i], e->phase_ev[i + 1]));
   });
+}
+
+hrt_status hrt_debug_trace(hrt_engine* eng, int64_t* out, int32_t n) {
+  return guarded(eng, [&] { eng->impl->debug_trace(out, n); });
 }
 
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable) {

@@ -129,6 +129,12 @@ class Engine:
         self._check(self.lib.hrt_phase_times(self._h, _ptr(ms, C.c_float)))
         return dict(encoder=float(ms[0]), stage1=float(ms[1]), stage2=float(ms[2]))
 
+    def debug_trace(self):
+        """ns stamps of the tail megakernel's phase barriers (option mega_trace)."""
+        buf = np.zeros(64, np.int64)
+        self._check(self.lib.hrt_debug_trace(self._h, _ptr(buf, C.c_int64), 64))
+        return buf
+
     def timing_enable(self, kernel_class="all", enable=True):
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 

@@ -334,3 +334,37 @@ def test_checkpoint_model_and_cli_translate(hrt, golden, tmp_path, capsys):
               os.path.join(here, "tiny_vocab.txt"), "--input", str(src), "--batch", "8"])
     lines = capsys.readouterr().out.strip().split("\n")
     assert lines == [" ".join(vocab[t] for t in r["out"]["tokens"]) for r in greedy]
+
+
+def test_tail_megakernel_matches_regular_path(hrt):
+    """Stage-I tail megakernel (<= 8 live rows, cooperative, GEMV phases) vs the
+    regular tcgen05 path on a d=256/dh=64 model: same decoder calls, tokens
+    agree (bf16 rounding differs only in summation order), and both track the
+    fp64 oracle."""
+    from paper_2212_01543_b200 import workload as W
+
+    cfg = hrt.ModelConfig(d_model=256, d_ff=512, n_heads=4, enc_layers=2, dec_layers=2, vocab_size=2000, max_len=64)
+    model = hrt.HRTModel.random(cfg, 33)
+    srcs = W.make_sources(12, 44, ("uniform", 3, 40), vocab_size=2000)
+    caps = W.stage1_caps(srcs, 2)
+    eng = hrt.Engine(model, dtype="bfloat16", max_sentences=16, max_beam=1)
+    eng.set_option("mega", 1)
+    a = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("mega", 0)
+    b = eng.translate_batch(srcs, 2, max_steps=caps)
+    agree = tot = 0
+    for x, y in zip(a, b):
+        assert x.decoder_calls == y.decoder_calls
+        tot += max(len(x.tokens), len(y.tokens))
+        agree += sum(p == q for p, q in zip(x.tokens, y.tokens))
+        assert abs(x.score - y.score) <= 2e-2 * max(1.0, abs(y.score))
+    assert agree / tot > 0.95
+    ocfg = O.Config(256, 512, 4, 2, 2, 2000, 64)
+    orc = O.Oracle(ocfg, model.params, dtype=np.float64)
+    oa = ot = 0
+    for s, c, x in zip(srcs, caps, a):
+        ref = O.hrt_translate(orc, s, 2, max_steps=c)
+        ot += len(ref.tokens)
+        oa += sum(p == q for p, q in zip(x.tokens, ref.tokens))
+    print(f"megakernel bf16 token agreement vs fp64 oracle: {oa / ot:.4f}")
+    assert oa / ot > 0.9
