@@ -211,8 +211,12 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
-  bool use_mega = false;  // option "mega": Stage-I tail (<= MG_RMAX live rows) in the cooperative megakernel (measured: no faster than the graph path)
-  float *mg_qkv = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr, *mg_vpart = nullptr, *mg_veos = nullptr;
+  bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
+  bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
+  float4* mg_vpart = nullptr;
+  float* mg_veos = nullptr;
+  int mg_trace_step = 1;
+  int mg_skip = 0;  // debug option mega_skip (timing attribution only)
   unsigned* mg_bar = nullptr;
   unsigned long long* mg_trace = nullptr;  // debug option "mega_trace"
   bool mg_trace_on = false;
@@ -303,7 +307,7 @@ struct Engine : EngineBase {
     cudaFree(p_mem);
     cudaFree(sk_ws);
     cudaFree(sk_counters);
-    cudaFree(mg_qkv);
+    cudaFree(mg_q);
     cudaFree(mg_ctx);
     cudaFree(mg_hid);
     cudaFree(mg_vpart);
@@ -627,10 +631,10 @@ struct Engine : EngineBase {
     }
     stats.arena_bytes = (int64_t)(arena_bytes + pbytes);
     if (BF16) {
-      CUDA_OK(cudaMalloc(&mg_qkv, (size_t)MG_RMAX * 3 * d * sizeof(float)));
-      CUDA_OK(cudaMalloc(&mg_ctx, (size_t)MG_RMAX * d * sizeof(float)));
-      CUDA_OK(cudaMalloc(&mg_hid, (size_t)MG_RMAX * ff * sizeof(float)));
-      CUDA_OK(cudaMalloc(&mg_vpart, (size_t)MG_RMAX * num_sms * 4 * sizeof(float)));
+      CUDA_OK(cudaMalloc(&mg_q, (size_t)MG_RMAX * d * sizeof(bf16)));
+      CUDA_OK(cudaMalloc(&mg_ctx, (size_t)MG_RMAX * d * sizeof(bf16)));
+      CUDA_OK(cudaMalloc(&mg_hid, (size_t)MG_RMAX * ff * sizeof(bf16)));
+      CUDA_OK(cudaMalloc(&mg_vpart, (size_t)MG_RMAX * num_sms * sizeof(float4)));
       CUDA_OK(cudaMalloc(&mg_veos, MG_RMAX * sizeof(float)));
       CUDA_OK(cudaMalloc(&mg_bar, 2 * sizeof(unsigned)));
       CUDA_OK(cudaMemset(mg_bar, 0, 2 * sizeof(unsigned)));
@@ -1324,9 +1328,15 @@ struct Engine : EngineBase {
     }
   }
 
+  // prefetch slot depth (32-wide K chunks per warp) that fits the shared-memory budget
+  int mega_npf() const {
+    int npf = 8;
+    while (npf > 0 && mega_smem_bytes(d, ff, npf) > 227 * 1024) --npf;
+    return npf;
+  }
   bool mega_ok() const {
-    return BF16 && use_mega && dh == 64 && d % 256 == 0 && ff % 256 == 0 && Ld <= MG_MAX_LAYERS &&
-           timed_class == 0 && s1_skip == 0;
+    return BF16 && use_mega && dh == 64 && d % 128 == 0 && d <= 1024 && ff % 32 == 0 && Ld <= MG_MAX_LAYERS &&
+           timed_class == 0 && s1_skip == 0 && cap_max <= MG_THREADS && mega_npf() >= 1;
   }
   // Stage-I steps [t0, t1) in the cooperative tail megakernel (rows <= MG_RMAX)
   void launch_mega(int t0, int t1, int k, int nrows, const GreedyState& gs) {
@@ -1359,7 +1369,7 @@ struct Engine : EngineBase {
     mp.kc = reinterpret_cast<bf16*>(s1.kc);
     mp.vc = reinterpret_cast<bf16*>(s1.vc);
     mp.x = s1.x;
-    mp.qkv = mg_qkv;
+    mp.q = mg_q;
     mp.ctx = mg_ctx;
     mp.hid = mg_hid;
     mp.vpart = mg_vpart;
@@ -1372,8 +1382,11 @@ struct Engine : EngineBase {
     mp.t_end = t1;
     mp.nrows = nrows;
     mp.trace = mg_trace_on ? mg_trace : nullptr;
-    const size_t smem = ((size_t)MG_RMAX * std::max(d, ff) + (size_t)MG_WARPS * (cap_max + 4) +
-                         (size_t)MG_WARPS * MG_RMAX * 4) * sizeof(float);
+    mp.trace_step = t0 + mg_trace_step;
+    mp.skip = mg_skip;
+    mp.npf = mega_npf();
+    const size_t smem = mega_smem_bytes(d, ff, mp.npf);
+    CUDA_OK(cudaMemsetAsync(mg_bar, 0, sizeof(unsigned), stream));
     static bool attr = false;
     if (!attr) {
       CUDA_OK(cudaFuncSetAttribute(decode_mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1444,6 +1457,10 @@ struct Engine : EngineBase {
       use_splitk = value != 0;
     else if (name == "mega")
       use_mega = value != 0;
+    else if (name == "mega_trace_step")
+      mg_trace_step = value;
+    else if (name == "mega_skip")
+      mg_skip = value;
     else if (name == "mega_trace") {
       mg_trace_on = value != 0;
       if (mg_trace_on && !mg_trace) {

@@ -1,0 +1,13 @@
+"""One batch-1 fused decode with the persistent Stage-I kernel (for ncu)."""
+import sys, numpy as np
+sys.path.insert(0, "/root/repo")
+import paper_2212_01543_b200 as hrt
+from paper_2212_01543_b200 import workload as W
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+spec = W.CONFIGS["c2"]
+eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=max(B, 1), max_beam=1)
+srcs = W.make_sources(B, 1001, spec["lengths"])
+ids = np.concatenate([np.asarray(s, np.int32) for s in srcs]); lens = [len(s) for s in srcs]
+for _ in range(2):
+    eng.translate_arrays(ids, lens, k=2, max_steps=[30] * B)
+print(eng.phase_times())

@@ -3,7 +3,8 @@ sys.path.insert(0, "/root/repo")
 import paper_2212_01543_b200 as hrt
 from paper_2212_01543_b200 import workload as W
 spec = W.CONFIGS["c2"]
-eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=8, max_beam=1)
+eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=32, max_beam=1)
+eng.set_option("mega", 1)
 eng.set_option("mega_trace", 1)
 for B in (1, 8):
     srcs = W.make_sources(B, 1001, spec["lengths"])
