@@ -1,0 +1,251 @@
+// Small-M projections ("GEMV" regime) on mma.sync for the latency-bound
+// shapes: Stage-I decode steps at small live-row counts and the encoder /
+// Stage II at batch 1 (M <= 32 rows).
+//
+//     C[M, N] = A[M, K] . W[N, K]^T   (bf16 in, fp32 accumulate)
+//
+// At these shapes the tcgen05 tile (128 x BN, one TMA pipeline per CTA over
+// the whole K) leaves a handful of CTAs each streaming its weight panel
+// serially; here one CTA owns 16 output features and its 16 warps split K, so
+// every weight byte is requested by its own lane at kernel start (before the
+// PDL grid-dependency wait: weights never depend on the previous kernel).
+// Swap-AB mma.sync m16n8k16: the 16-feature weight tile is the M side, the
+// rows (8 per n-tile) the N side; the K index is permuted identically on both
+// operands (lane (g, t) holds k = 8t..8t+7 of each 32-wide chunk) so each
+// weight fragment is one 16-byte load. Partial sums are reduced across warps
+// in shared memory in a fixed order (deterministic), then warp 0 runs the
+// same element-wise epilogue functors as the tcgen05 GEMM (gemm_epi.cuh).
+//
+// gemv_vocab_kernel: the tied vocabulary projection (infer.py:293-301) with
+// the Stage-I statistics fused: a CTA covers 256 columns (16 warps x 16) and
+// emits one {max, sum exp, top-1 allowed} partial per row, in the VocabParts
+// layout the selection kernels merge.
+#pragma once
+#include "common.cuh"
+#include "gemm_epi.cuh"
+#include "kernels.cuh"
+
+namespace hrt {
+
+constexpr int GV_WARPS = 16;
+constexpr int GV_THREADS = GV_WARPS * 32;
+constexpr int GV_MAXC = 8;  // K-chunks (32 wide) per warp held in registers (K <= 4096)
+
+__device__ __forceinline__ void gv_mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint4 gv_ldw(const bf16* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <int NT, int CPW, class Epi>
+__global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __restrict__ A, int lda,
+                                                                const bf16* __restrict__ W, int N, int K, int M,
+                                                                const int* __restrict__ M_dev, Epi epi) {
+  __shared__ float red[GV_WARPS][NT * 4][32];
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int n0 = blockIdx.x * 16;
+  const int nch = K / 32;  // == GV_WARPS * CPW, or fewer chunks than warps with CPW == 1
+  const int c0 = warp * CPW, c1 = min(c0 + CPW, nch);
+  const int nvalid = N - n0;
+  const bf16* w0 = W + (size_t)(n0 + min(g, nvalid - 1)) * K + t4 * 8;
+  const bf16* w1 = W + (size_t)(n0 + min(g + 8, nvalid - 1)) * K + t4 * 8;
+  // weight fragments: unconditional (clamped) loads keep the arrays in registers
+  uint4 u0[CPW], u1[CPW];
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int ch = min(c0 + i, nch - 1);
+    u0[i] = gv_ldw(w0 + 32 * ch);
+    u1[i] = gv_ldw(w1 + 32 * ch);
+  }
+  pdl_wait();
+  if (M_dev) M = *M_dev;
+  float c[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
+  // activation (B) fragments: row 8j+g, k = 32 ch + 8 t
+  const bf16* a = A + t4 * 8;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    if (c0 + i < c1) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int r = min(8 * j + g, M - 1);
+        const uint4 v = *reinterpret_cast<const uint4*>(a + (size_t)r * lda + 32 * (c0 + i));
+        gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
+        gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[warp][j * 4 + e][lane] = c[j][e];
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float s = red[0][j * 4 + e][lane];
+      for (int w = 1; w < GV_WARPS; ++w) s += red[w][j * 4 + e][lane];
+      c[j][e] = s;
+    }
+  const int f0 = n0 + g, f1 = f0 + 8;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int r0 = 8 * j + 2 * t4;
+    if (r0 < M) {
+      if (f0 < N) epi.apply1(r0, f0, c[j][0]);
+      if (f1 < N) epi.apply1(r0, f1, c[j][2]);
+    }
+    if (r0 + 1 < M) {
+      if (f0 < N) epi.apply1(r0 + 1, f0, c[j][1]);
+      if (f1 < N) epi.apply1(r0 + 1, f1, c[j][3]);
+    }
+  }
+}
+
+// online {max, sum exp} + top-1 (value desc, id asc) over the generable set
+struct GvStat {
+  float mx, sum, bv;
+  int bi;
+  __device__ __forceinline__ void init() {
+    mx = -INFINITY;
+    sum = 0.f;
+    bv = -INFINITY;
+    bi = 0x7fffffff;
+  }
+  __device__ __forceinline__ void add(float l, int v, int norm_allowed) {
+    const bool ok = id_allowed(v);
+    if (ok && better(l, v, bv, bi)) {
+      bv = l;
+      bi = v;
+    }
+    if (norm_allowed && !ok) return;
+    if (l > mx) {
+      sum = sum * ex2f((mx - l) * LOG2E) + 1.f;
+      mx = l;
+    } else {
+      sum += ex2f((l - mx) * LOG2E);
+    }
+  }
+  __device__ __forceinline__ void merge(float om, float os, float obv, int obi) {
+    if (om != -INFINITY) {
+      const float m = fmaxf(mx, om);
+      sum = (mx == -INFINITY ? 0.f : sum * ex2f((mx - m) * LOG2E)) + os * ex2f((om - m) * LOG2E);
+      mx = m;
+    }
+    if (better(obv, obi, bv, bi)) {
+      bv = obv;
+      bi = obi;
+    }
+  }
+};
+
+constexpr int GV_VTILE = GV_WARPS * 16;  // vocabulary columns per CTA (one partial per row)
+
+// Vocabulary statistics for M <= 8 * NT rows (KT = 1: greedy selection and
+// the Stage-II argmax): parts.ntiles must be cdiv(V, GV_VTILE).
+template <int NT>
+__global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
+                                                                const bf16* __restrict__ E, int V, int K, int M,
+                                                                const int* __restrict__ M_dev, VocabParts parts,
+                                                                int norm_allowed) {
+  __shared__ float4 ws[GV_WARPS][8 * NT];
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int n0 = blockIdx.x * GV_VTILE + warp * 16;
+  const int nch = K / 32;
+  const int nvalid = V - n0;
+  const bool has = nvalid > 0;
+  const bf16* w0 = E + (size_t)max(0, min(n0 + g, V - 1)) * K + t4 * 8;
+  const bf16* w1 = E + (size_t)max(0, min(n0 + g + 8, V - 1)) * K + t4 * 8;
+  // first batch of weight fragments before the grid-dependency wait
+  uint4 u0[GV_MAXC], u1[GV_MAXC];
+#pragma unroll
+  for (int i = 0; i < GV_MAXC; ++i) {
+    const int ch = min(i, nch - 1);
+    u0[i] = gv_ldw(w0 + 32 * ch);
+    u1[i] = gv_ldw(w1 + 32 * ch);
+  }
+  pdl_wait();
+  if (M_dev) M = *M_dev;
+  float c[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
+  const bf16* a = A + t4 * 8;
+  for (int cb = 0; cb < nch; cb += GV_MAXC) {
+    if (cb > 0) {
+#pragma unroll
+      for (int i = 0; i < GV_MAXC; ++i) {
+        const int ch = min(cb + i, nch - 1);
+        u0[i] = gv_ldw(w0 + 32 * ch);
+        u1[i] = gv_ldw(w1 + 32 * ch);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < GV_MAXC; ++i) {
+      if (cb + i < nch) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int r = min(8 * j + g, M - 1);
+          const uint4 v = *reinterpret_cast<const uint4*>(a + (size_t)r * lda + 32 * (cb + i));
+          gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
+          gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
+        }
+      }
+    }
+  }
+  // per-row statistics of this warp's 16 columns, merged over the 8 lanes sharing the rows
+  const int f0 = n0 + g, f1 = f0 + 8;
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      GvStat s;
+      s.init();
+      if (has && f0 < V) s.add(c[j][e], f0, norm_allowed);
+      if (has && f1 < V) s.add(c[j][2 + e], f1, norm_allowed);
+      const int row = 8 * j + 2 * t4 + e;
+      if (f0 == EOS_ID && row < M) parts.eos[row] = c[j][e];
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, s.mx, o);
+        const float os = __shfl_xor_sync(0xffffffffu, s.sum, o);
+        const float ov = __shfl_xor_sync(0xffffffffu, s.bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, s.bi, o);
+        s.merge(om, os, ov, oi);
+      }
+      if (g == 0) ws[warp][8 * j + 2 * t4 + e] = make_float4(s.mx, s.sum, s.bv, __int_as_float(s.bi));
+    }
+  __syncthreads();
+  if ((int)threadIdx.x < M) {
+    const int r = threadIdx.x;
+    GvStat s;
+    s.init();
+#pragma unroll 4
+    for (int w = 0; w < GV_WARPS; ++w) {
+      const float4 v = ws[w][r];
+      s.merge(v.x, v.y, v.z, __float_as_int(v.w));
+    }
+    const size_t o = (size_t)r * parts.ntiles + blockIdx.x;
+    parts.mx[o] = s.mx;
+    parts.sum[o] = s.sum;
+    parts.val[o] = s.bv;
+    parts.id[o] = s.bi;
+  }
+}
+
+}  // namespace hrt

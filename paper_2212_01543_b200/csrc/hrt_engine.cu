@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "gemm_epi.cuh"
 #include "gemm_simt.cuh"
+#include "gemv_small.cuh"
 #include "kernels.cuh"
 #include "decode_mega.cuh"
 #include "tc_gemm.cuh"
@@ -211,6 +212,7 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
+  bool use_attn_heads = true;  // option "attn_heads": all-heads-per-CTA prefill attention
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
   float4* mg_vpart = nullptr;
@@ -703,6 +705,38 @@ struct Engine : EngineBase {
     return 64;
   }
 
+  // small-M regime (decode steps at small batch, batch-1 encoder / Stage II):
+  // mma.sync GEMV with K split over the warps of a CTA (gemv_small.cuh)
+  bool use_gemv = true;  // option "gemv"
+  static constexpr int GEMV_MAX_M = 32;
+  // path_rows: when set (eager Stage-I loop), the kernel choice follows the
+  // captured graph's row bucket instead of the live row count, so eager and
+  // graph launches run the same kernels (bit-identical results)
+  int path_rows = 0;
+  bool gemv_ok(int M, int K) const {
+    const int Mp = path_rows > 0 ? path_rows : M;
+    return use_gemv && Mp <= GEMV_MAX_M && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
+  }
+  template <int NT, int CPW, class Epi>
+  void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+    launch(gemv_small_kernel<NT, CPW, Epi>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A), lda,
+           reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi);
+  }
+  template <int NT, class Epi>
+  void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+    const int cpw = std::max(1, K / 32 / GV_WARPS);
+    if (cpw == 1) gemv_launch_t<NT, 1>(A, lda, M, W, N, K, epi, M_dev);
+    else if (cpw == 2) gemv_launch_t<NT, 2>(A, lda, M, W, N, K, epi, M_dev);
+    else if (cpw == 4) gemv_launch_t<NT, 4>(A, lda, M, W, N, K, epi, M_dev);
+    else gemv_launch_t<NT, 8>(A, lda, M, W, N, K, epi, M_dev);
+  }
+  template <class Epi>
+  void gemv_launch(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+    if (M <= 8) gemv_launch_n<1>(A, lda, M, W, N, K, epi, M_dev);
+    else if (M <= 16) gemv_launch_n<2>(A, lda, M, W, N, K, epi, M_dev);
+    else gemv_launch_n<4>(A, lda, M, W, N, K, epi, M_dev);
+  }
+
   // C[M,N] = A[M,K] . W[N,K]^T with a fused epilogue
   template <class Epi>
   void gemm(int cls, const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi,
@@ -710,6 +744,11 @@ struct Engine : EngineBase {
     if (M <= 0) return;
     Scope sc(this, cls, (double)sizeof(T) * ((double)N * K + (double)M * K), 2.0 * M * N * K);
     if constexpr (BF16) {
+      if (gemv_ok(M, K)) {
+        gemv_launch(A, lda, M, W, N, K, epi, M_dev);
+        check_launch();
+        return;
+      }
       if (bn == 0) bn = choose_bn(M, N);
       if (bn == 64)
         tc_launch<64, 8>(A, a_cap, lda, M, W, N, K, epi, M_dev);
@@ -810,6 +849,20 @@ struct Engine : EngineBase {
     const int2* it2 = reinterpret_cast<const int2*>(items);
 #define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
     if constexpr (BF16) {
+      if (dh == 64 && H <= 8 && use_attn_heads) {
+        // all heads per CTA (K/V rows fetched once, cp.async + ldmatrix.trans)
+        const size_t smem = attn_heads_smem(d);
+        static bool attr = false;
+        if (!attr) {
+          CUDA_OK(cudaFuncSetAttribute(attn_prefill_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn_heads_smem(512)));
+          attr = true;
+        }
+        launch(attn_prefill_heads_kernel, dim3(n_items), 2 * H * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off,
+               q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal, att_scale, H);
+        check_launch();
+        return;
+      }
       if (dh == 64) {
         launch(attn_prefill_mma_kernel, grid, AM_WARPS * 32, 0, it2, q, qs, k, v, kvs, out, os, q_off, q_slot,
                                                                    q_len, kv_map, kv_off, kv_len, key_ok, causal,
@@ -864,6 +917,20 @@ struct Engine : EngineBase {
                    const int* M_dev = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
+      if (kt == 1 && gemv_ok(R, d)) {
+        parts.ntiles = cdiv(V, GV_VTILE);
+        Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
+        const bf16* yb = reinterpret_cast<const bf16*>(y);
+        const bf16* Eb = reinterpret_cast<const bf16*>(E);
+        if (R <= 8)
+          launch(gemv_vocab_kernel<1>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+        else if (R <= 16)
+          launch(gemv_vocab_kernel<2>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+        else
+          launch(gemv_vocab_kernel<4>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+        check_launch();
+        return;
+      }
       const int bn = vocab_bn(R);
       parts.ntiles = cdiv(V, bn / 2);  // one partial per epilogue column half
       Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
@@ -1457,6 +1524,16 @@ struct Engine : EngineBase {
       use_splitk = value != 0;
     else if (name == "mega")
       use_mega = value != 0;
+    else if (name == "attn_heads")
+      use_attn_heads = value != 0;
+    else if (name == "gemv") {
+      use_gemv = value != 0;
+      for (auto& kv : loop_graphs) {  // captured loops bake the GEMM path in
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      }
+      loop_graphs.clear();
+    }
     else if (name == "mega_trace_step")
       mg_trace_step = value;
     else if (name == "mega_skip")
@@ -1746,26 +1823,38 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     t_mega = 0;
     while (t_mega < max_cap && alive[t_mega] > MG_RMAX) ++t_mega;
   }
-  if (t_mega > 0) {
-    if (t_mega < max_cap) {  // the regular loop stops where the megakernel takes over
-      StepCtl c{0, alive[0], 0, k, t_mega, B, 0, 0};
-      CUDA_OK(cudaMemcpyAsync(s_ctl, &c, sizeof(StepCtl), cudaMemcpyHostToDevice, stream));
+  // Stage-I steps in segments of constant row bucket (power of two >= live
+  // rows): each segment is one launch of its bucket's captured loop graph, so
+  // kernel choice and grid size follow the shrinking batch (small buckets take
+  // the mma.sync GEMV path)
+  auto bucket_of = [&](int r) {
+    int b = 1;
+    while (b < r) b <<= 1;
+    return std::min(b, R_max);
+  };
+  for (int t0 = 0; t0 < t_mega && alive[t0] > 0;) {
+    const int bucket = bucket_of(alive[t0]);
+    int t1 = t0;
+    while (t1 < t_mega && alive[t1] > 0 && bucket_of(alive[t1]) == bucket) ++t1;
+    if (t0 > 0 || t1 < max_cap) {  // loop control for this segment (the finished count carries over)
+      const int hdr[5] = {t0, alive[t0], t0 * k, k, t1};
+      CUDA_OK(cudaMemcpyAsync(s_ctl, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream));
     }
     if (BF16 && use_graphs && timed_class == 0) {
-      // the whole Stage-I loop as ONE graph launch (conditional WHILE node)
-      int bucket = 1;
-      while (bucket < B * beam) bucket <<= 1;
-      bucket = std::min(bucket, R_max);
       LoopGraph& lg = loop_graph(bucket, beam, gs, bs);
       CUDA_OK(cudaGraphLaunch(lg.exec, stream));
-      stats.kernel_launches += (int64_t)lg.kernels * t_mega;
+      stats.kernel_launches += (int64_t)lg.kernels * (t1 - t0);
     } else {
-      for (int t = 0; t < t_mega; ++t) {
-        const int R = alive[t];
-        if (R == 0) break;
-        stage1_step(R, t, k, beam, max_src, d_off, d_len, gs, bs, nullptr);
+      path_rows = bucket;  // same kernel choices as the captured loop
+      try {
+        for (int t = t0; t < t1; ++t) stage1_step(alive[t], t, k, beam, max_src, d_off, d_len, gs, bs, nullptr);
+      } catch (...) {
+        path_rows = 0;
+        throw;
       }
+      path_rows = 0;
     }
+    t0 = t1;
   }
   if (t_mega < max_cap) launch_mega(t_mega, max_cap, k, B, gs);
   phase_mark(2);

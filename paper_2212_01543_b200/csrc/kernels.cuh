@@ -504,6 +504,189 @@ __global__ void __launch_bounds__(AM_WARPS * 32) attn_prefill_mma_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// All-heads variant of the bf16 prefill attention (d_head = 64, heads <= 8):
+// one CTA per (sequence, 32-query block) covers every head, so K/V rows are
+// fetched once as whole d-wide rows with cp.async (1 KB contiguous per key at
+// d = 512) instead of once per head. Warp 2h + i owns head h, queries
+// 16i..16i+15; QK^T and PV on mma.sync m16n8k16, V fragments by
+// ldmatrix.trans (no scalar transpose), online softmax over 32-key chunks.
+// Same item list, masks and output contract as attn_prefill_mma_kernel.
+// ---------------------------------------------------------------------------
+constexpr int AH_KC = 32, AH_PAD = 8;
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+
+inline size_t attn_heads_smem(int d) { return (size_t)(32 + 2 * AH_KC) * (d + AH_PAD) * 2 + AH_KC * sizeof(float); }
+
+__global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
+    const int2* __restrict__ items, const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ k,
+    const bf16* __restrict__ v, int kv_stride, bf16* __restrict__ out, int out_stride, const int* __restrict__ q_off,
+    const int* __restrict__ q_slot, const int* __restrict__ q_len, const int* __restrict__ kv_map,
+    const int* __restrict__ kv_off, const int* __restrict__ kv_len, const unsigned char* __restrict__ key_ok,
+    int causal, float scale, int H) {
+  pdl_enter();
+  constexpr int DH = 64;
+  extern __shared__ __align__(16) unsigned char ah_raw[];
+  const int d = H * DH, ld = d + AH_PAD, c8n = d / 8;
+  bf16* Qs = reinterpret_cast<bf16*>(ah_raw);
+  bf16* Ks = Qs + 32 * ld;
+  bf16* Vs = Ks + AH_KC * ld;
+  float* kbias = reinterpret_cast<float*>(Vs + AH_KC * ld);
+  const int2 it = items[blockIdx.x];
+  const int s = it.x, qbeg = it.y * 32;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int qslot = q_slot[s], qlen = q_len[s];
+  const int kvs = kv_map ? kv_map[s] : s;
+  const int kb = kv_off[kvs], L = kv_len[kvs], qb = q_off[s];
+  // Q block (rows past q_len zero-filled)
+  for (int idx = tid; idx < 32 * c8n; idx += nthr) {
+    const int r = idx / c8n, c = (idx - r * c8n) * 8;
+    const bool ok = qbeg + r < qlen;
+    cp_async16_zfill(Qs + r * ld + c, q + (size_t)(qb + (ok ? qbeg + r : 0)) * q_stride + c, ok);
+  }
+  const int h = warp >> 1, qh = warp & 1, hoff = h * DH;
+  const int g = lane >> 2, tq = lane & 3;
+  const int qi0 = qbeg + qh * 16 + g, qi1 = qi0 + 8;
+  float o[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = scale * LOG2E;
+  const int qmax = min(qslot, qbeg + 32) - 1;
+  const int Lc = causal ? min(L, qmax + 1) : L;
+  uint32_t qa[4][4];
+  for (int j0 = 0; j0 < Lc; j0 += AH_KC) {
+    const int nk = min(AH_KC, Lc - j0);
+    if (j0 > 0) __syncthreads();  // previous chunk consumed
+    for (int idx = tid; idx < AH_KC * c8n; idx += nthr) {
+      const int j = idx / c8n, c = (idx - j * c8n) * 8;
+      const bool ok = j < nk;
+      const size_t r = (size_t)(kb + j0 + (ok ? j : 0)) * kv_stride + c;
+      cp_async16_zfill(Ks + j * ld + c, k + r, ok);
+      cp_async16_zfill(Vs + j * ld + c, v + r, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int j = tid; j < AH_KC; j += nthr)
+      kbias[j] = (j < nk && (key_ok == nullptr || key_ok[kb + j0 + j])) ? 0.f : -INFINITY;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    {  // Q fragments re-read from shared memory each chunk (keeps registers for two CTAs per SM)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int c = hoff + ks * 16 + tq * 2;
+        const bf16* q0 = Qs + (qh * 16 + g) * ld + c;
+        const bf16* q1 = q0 + 8 * ld;
+        qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0);
+        qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1);
+        qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + 8);
+        qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + 8);
+      }
+    }
+    // S = Q K^T: 16 queries x 32 keys (4 n-tiles of 8 keys)
+    float sc[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+      const bf16* kr = Ks + (n * 8 + g) * ld + hoff + tq * 2;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t b[2];
+        b[0] = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
+        b[1] = *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8);
+        mma_bf16_16816(sc[n], qa[ks], b);
+      }
+    }
+    // mask + online softmax (base 2)
+    float cm0 = -INFINITY, cm1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = n * 8 + tq * 2 + e;
+        const float kbj = kbias[j];
+        float a0 = sc[n][e] * sl2 + kbj, a1 = sc[n][2 + e] * sl2 + kbj;
+        if (causal && j0 + j > qi0) a0 = -INFINITY;
+        if (causal && j0 + j > qi1) a1 = -INFINITY;
+        sc[n][e] = a0;
+        sc[n][2 + e] = a1;
+        cm0 = fmaxf(cm0, a0);
+        cm1 = fmaxf(cm1, a1);
+      }
+    }
+    cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, 1));
+    cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, 2));
+    cm1 = fmaxf(cm1, __shfl_xor_sync(0xffffffffu, cm1, 1));
+    cm1 = fmaxf(cm1, __shfl_xor_sync(0xffffffffu, cm1, 2));
+    const float mn0 = fmaxf(m0, cm0), mn1 = fmaxf(m1, cm1);
+    const float b0 = mn0 == -INFINITY ? 0.f : mn0, b1 = mn1 == -INFINITY ? 0.f : mn1;
+    const float c0 = ex2f(m0 - b0), c1 = ex2f(m1 - b1);
+    m0 = mn0;
+    m1 = mn1;
+    float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      sc[n][0] = ex2f(sc[n][0] - b0);
+      sc[n][1] = ex2f(sc[n][1] - b0);
+      sc[n][2] = ex2f(sc[n][2] - b1);
+      sc[n][3] = ex2f(sc[n][3] - b1);
+      ps0 += sc[n][0] + sc[n][1];
+      ps1 += sc[n][2] + sc[n][3];
+    }
+    l0 = l0 * c0 + ps0;
+    l1 = l1 * c1 + ps1;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      o[n][0] *= c0;
+      o[n][1] *= c0;
+      o[n][2] *= c1;
+      o[n][3] *= c1;
+    }
+    // O += P V: P fragments from the score accumulators, V fragments by ldmatrix.trans
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sc[2 * ks][0], sc[2 * ks][1]);
+      pa[1] = pack_bf16(sc[2 * ks][2], sc[2 * ks][3]);
+      pa[2] = pack_bf16(sc[2 * ks + 1][0], sc[2 * ks + 1][1]);
+      pa[3] = pack_bf16(sc[2 * ks + 1][2], sc[2 * ks + 1][3]);
+#pragma unroll
+      for (int n = 0; n < 8; n += 2) {
+        // lanes 0-15: keys ks*16 + lane, dims n*8..; lanes 16-31: same keys, dims (n+1)*8..
+        const bf16* vp = Vs + (ks * 16 + (lane & 15)) * ld + hoff + (n + (lane >> 4)) * 8;
+        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(vp));
+        uint32_t b[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                     : "r"(sa));
+        mma_bf16_16816(o[n], pa, b);
+        mma_bf16_16816(o[n + 1], pa, b + 2);
+      }
+    }
+  }
+  if (Lc <= 0) __syncthreads();  // (no chunk ran: keep the Q copy's barrier discipline)
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = (qi0 < qlen && l0 > 0.f) ? 1.f / l0 : 0.f;
+  const float i1 = (qi1 < qlen && l1 > 0.f) ? 1.f / l1 : 0.f;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const int c = hoff + n * 8 + tq * 2;
+    if (qi0 < qslot)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(qb + qi0) * out_stride + c) =
+          __floats2bfloat162_rn(o[n][0] * i0, o[n][1] * i0);
+    if (qi1 < qslot)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(qb + qi1) * out_stride + c) =
+          __floats2bfloat162_rn(o[n][2] * i1, o[n][3] * i1);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Single-query attention for one Stage-I decoder step (infer.py:259-285).
 // SELF: append this step's k/v at cache slot t, then attend slots 0..t of the
 //       row's history; history slot j of logical row r lives in physical row

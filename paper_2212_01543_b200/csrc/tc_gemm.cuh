@@ -97,12 +97,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
-  if (M_dev != nullptr) M = *M_dev;
-  const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (N + BN - 1) / BN;
   // work unit = (tile, k-slice); sk.splits > 1 only for element-wise epilogues
   const int S = sk.splits;
+  // Weights do not depend on the previous kernel: the first unit of a CTA in
+  // m-tile 0 (which exists for any M >= 1) gets its first STAGES weight tiles
+  // requested before the grid-dependency wait, overlapping the previous
+  // kernel's tail (the A tiles follow after the wait into the same stages).
+  int pre = 0;
+  if (warp == 0 && lane == 0 && (int)blockIdx.x < n_tiles * S) {
+    const int tile = blockIdx.x / S, ks = blockIdx.x - tile * S;
+    const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
+    pre = min(STAGES, kb1 - kb0);
+    const uint64_t pol = policy_evict_last();
+    for (int s2 = 0; s2 < pre; ++s2) {
+      mbar_arrive_expect_tx(&full[s2], L::STAGE_BYTES);
+      tma_load_2d_hint(smem + s2 * L::STAGE_BYTES + L::A_BYTES, &tmB, &full[s2], (kb0 + s2) * TC_BK, tile * BN, pol);
+    }
+  }
+  pdl_wait();
+  if (M_dev != nullptr) M = *M_dev;
+  const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int num_units = m_tiles * n_tiles * S;
 
   if (warp == 0) {
@@ -118,9 +133,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
-          tma_load_2d_hint(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, pol_w);
+          if (u == (int)blockIdx.x && kb - kb0 < pre) {  // weight tile already requested before the PDL wait
+            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
+            tma_load_2d_hint(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, pol_w);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;

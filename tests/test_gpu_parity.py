@@ -368,3 +368,25 @@ def test_tail_megakernel_matches_regular_path(hrt):
         oa += sum(p == q for p, q in zip(x.tokens, ref.tokens))
     print(f"megakernel bf16 token agreement vs fp64 oracle: {oa / ot:.4f}")
     assert oa / ot > 0.9
+
+
+def test_prefill_attention_all_heads_matches_per_head_kernel(hrt, golden):
+    """All-heads-per-CTA prefill attention (cp.async + ldmatrix.trans) vs the
+    per-head mma.sync kernel: encoder memory and Stage-II logits agree to bf16
+    rounding, decoded tokens agree."""
+    g = golden("dh64")
+    sess = hrt.CudaSession(_model(hrt, g), dtype="bfloat16", max_sentences=8)
+    v = g["vectors"]
+    pos = np.arange(1, len(v["ids"]) + 1)[None, :]
+    res = {}
+    for on in (1, 0):
+        sess.engine.set_option("attn_heads", on)
+        mem = np.array(sess.encode(v["src"]))
+        full = np.array(sess.parallel_logits([v["ids"]], pos, "full")[0])
+        causal = np.array(sess.parallel_logits([v["ids"]], pos, "causal")[0])
+        toks = [t.tokens for t in hrt.hrt_translate_batch(sess, g["sources"], 2)]
+        res[on] = (mem, full, causal, toks)
+    for a, b in zip(res[1][:3], res[0][:3]):
+        assert _rel(a, b) < 2e-2
+    agree = sum(x == y for x, y in zip(res[1][3], res[0][3]))
+    assert agree >= len(g["sources"]) - 1
