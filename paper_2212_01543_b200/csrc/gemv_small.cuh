@@ -40,19 +40,86 @@ __device__ __forceinline__ void gv_mma(float (&c)[4], uint32_t a0, uint32_t a1, 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint4 gv_ldw(const bf16* p) {
+// weight fragment load: read-only path, no L1 allocation, L2 evict-last (the
+// decoder + vocabulary weights, ~40 MB in bf16, stay L2-resident across steps)
+__device__ __forceinline__ uint64_t gv_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 gv_ldw(const bf16* p, uint64_t pol) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return v;
 }
 
-template <int NT, int CPW, class Epi>
+// Optional LayerNorm prologue (the activation operand is LN(x) of fp32 rows,
+// kernels.py:42-57): the CTA computes every row's statistics exactly as
+// layernorm_vec_kernel does (same lane partition and reduction order, so the
+// bf16 operand is bit-identical to the unfused LN kernel's output) and
+// normalises the 8-element fragments it feeds the MMA.
+struct GvLN {
+  const float* x;  // [M][K] fp32 rows (nullptr: A is the bf16 operand)
+  const float* g;
+  const float* b;
+};
+
+__device__ __forceinline__ void gv_ln_stats(const GvLN& ln, int M, int K, float2* st) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = K / 128;
+  for (int r = warp; r < M; r += GV_WARPS) {
+    const float4* xr = reinterpret_cast<const float4*>(ln.x + (size_t)r * K);
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < nv ? xr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = warp_sum(s) / K;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) {
+        const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+        q += (a * a + bb * bb) + (c * c + e * e);
+      }
+    const float inv = 1.0f / sqrtf(warp_sum(q) / K + 1e-5f);
+    if (lane == 0) st[r] = make_float2(mean, inv);
+  }
+}
+
+// bf16 operand fragment: 8 consecutive k of row r (LN applied when ln.x != nullptr)
+template <bool LNA>
+__device__ __forceinline__ uint4 gv_afrag(const bf16* A, int lda, const GvLN& ln, const float2* st, int K, int r,
+                                          int k0) {
+  if (!LNA) return *reinterpret_cast<const uint4*>(A + (size_t)r * lda + k0);
+  const float4* xp = reinterpret_cast<const float4*>(ln.x + (size_t)r * K + k0);
+  const float4* gp = reinterpret_cast<const float4*>(ln.g + k0);
+  const float4* bp = reinterpret_cast<const float4*>(ln.b + k0);
+  const float2 mi = st[r];
+  uint4 u;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float4 x = xp[h], g = __ldg(gp + h), b = __ldg(bp + h);
+    __nv_bfloat162 lo = __floats2bfloat162_rn((x.x - mi.x) * mi.y * g.x + b.x, (x.y - mi.x) * mi.y * g.y + b.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn((x.z - mi.x) * mi.y * g.z + b.z, (x.w - mi.x) * mi.y * g.w + b.w);
+    w[2 * h] = *reinterpret_cast<uint32_t*>(&lo);
+    w[2 * h + 1] = *reinterpret_cast<uint32_t*>(&hi);
+  }
+  return u;
+}
+
+template <int NT, int CPW, class Epi, bool LNA = false>
 __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ W, int N, int K, int M,
-                                                                const int* __restrict__ M_dev, Epi epi) {
-  __shared__ float red[GV_WARPS][NT * 4][32];
+                                                                const int* __restrict__ M_dev, Epi epi, GvLN ln) {
+  constexpr int NG = NT < 4 ? NT : 4;  // n-tiles reduced per shared-memory pass
+  __shared__ float red[GV_WARPS][NG * 4][32];
+  __shared__ float2 lnst[LNA ? 8 * NT : 1];
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
   const int n0 = blockIdx.x * 16;
@@ -62,46 +129,57 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   const bf16* w0 = W + (size_t)(n0 + min(g, nvalid - 1)) * K + t4 * 8;
   const bf16* w1 = W + (size_t)(n0 + min(g + 8, nvalid - 1)) * K + t4 * 8;
   // weight fragments: unconditional (clamped) loads keep the arrays in registers
+  const uint64_t pol = gv_policy();
   uint4 u0[CPW], u1[CPW];
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     const int ch = min(c0 + i, nch - 1);
-    u0[i] = gv_ldw(w0 + 32 * ch);
-    u1[i] = gv_ldw(w1 + 32 * ch);
+    u0[i] = gv_ldw(w0 + 32 * ch, pol);
+    u1[i] = gv_ldw(w1 + 32 * ch, pol);
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
+  if (LNA) {
+    gv_ln_stats(ln, M, K, lnst);
+    __syncthreads();
+  }
   float c[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
   // activation (B) fragments: row 8j+g, k = 32 ch + 8 t
-  const bf16* a = A + t4 * 8;
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     if (c0 + i < c1) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         const int r = min(8 * j + g, M - 1);
-        const uint4 v = *reinterpret_cast<const uint4*>(a + (size_t)r * lda + 32 * (c0 + i));
+        const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (c0 + i) + t4 * 8);
         gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
         gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
       }
     }
   }
+  // fixed-order reduction over the warps, NG n-tiles per pass
 #pragma unroll
-  for (int j = 0; j < NT; ++j)
+  for (int j0 = 0; j0 < NT; j0 += NG) {
+    if (j0 > 0) __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 4; ++e) red[warp][j * 4 + e][lane] = c[j][e];
-  __syncthreads();
-  if (warp != 0) return;
+    for (int j = 0; j < NG; ++j)
 #pragma unroll
-  for (int j = 0; j < NT; ++j)
+      for (int e = 0; e < 4; ++e) red[warp][j * 4 + e][lane] = c[j0 + j][e];
+    __syncthreads();
+    if (warp == 0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float s = red[0][j * 4 + e][lane];
-      for (int w = 1; w < GV_WARPS; ++w) s += red[w][j * 4 + e][lane];
-      c[j][e] = s;
+      for (int j = 0; j < NG; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float s = red[0][j * 4 + e][lane];
+          for (int w = 1; w < GV_WARPS; ++w) s += red[w][j * 4 + e][lane];
+          c[j0 + j][e] = s;
+        }
     }
+  }
+  if (warp != 0) return;
   const int f0 = n0 + g, f1 = f0 + 8;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -158,12 +236,13 @@ constexpr int GV_VTILE = GV_WARPS * 16;  // vocabulary columns per CTA (one part
 
 // Vocabulary statistics for M <= 8 * NT rows (KT = 1: greedy selection and
 // the Stage-II argmax): parts.ntiles must be cdiv(V, GV_VTILE).
-template <int NT>
+template <int NT, bool LNA = false>
 __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ E, int V, int K, int M,
                                                                 const int* __restrict__ M_dev, VocabParts parts,
-                                                                int norm_allowed) {
+                                                                int norm_allowed, GvLN ln) {
   __shared__ float4 ws[GV_WARPS][8 * NT];
+  __shared__ float2 lnst[LNA ? 8 * NT : 1];
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
   const int n0 = blockIdx.x * GV_VTILE + warp * 16;
@@ -173,26 +252,30 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
   const bf16* w0 = E + (size_t)max(0, min(n0 + g, V - 1)) * K + t4 * 8;
   const bf16* w1 = E + (size_t)max(0, min(n0 + g + 8, V - 1)) * K + t4 * 8;
   // first batch of weight fragments before the grid-dependency wait
+  const uint64_t pol = gv_policy();
   uint4 u0[GV_MAXC], u1[GV_MAXC];
 #pragma unroll
   for (int i = 0; i < GV_MAXC; ++i) {
     const int ch = min(i, nch - 1);
-    u0[i] = gv_ldw(w0 + 32 * ch);
-    u1[i] = gv_ldw(w1 + 32 * ch);
+    u0[i] = gv_ldw(w0 + 32 * ch, pol);
+    u1[i] = gv_ldw(w1 + 32 * ch, pol);
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
+  if (LNA) {
+    gv_ln_stats(ln, M, K, lnst);
+    __syncthreads();
+  }
   float c[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
-  const bf16* a = A + t4 * 8;
   for (int cb = 0; cb < nch; cb += GV_MAXC) {
     if (cb > 0) {
 #pragma unroll
       for (int i = 0; i < GV_MAXC; ++i) {
         const int ch = min(cb + i, nch - 1);
-        u0[i] = gv_ldw(w0 + 32 * ch);
-        u1[i] = gv_ldw(w1 + 32 * ch);
+        u0[i] = gv_ldw(w0 + 32 * ch, pol);
+        u1[i] = gv_ldw(w1 + 32 * ch, pol);
       }
     }
 #pragma unroll
@@ -201,7 +284,7 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int r = min(8 * j + g, M - 1);
-          const uint4 v = *reinterpret_cast<const uint4*>(a + (size_t)r * lda + 32 * (cb + i));
+          const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (cb + i) + t4 * 8);
           gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
           gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
         }

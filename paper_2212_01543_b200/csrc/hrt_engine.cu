@@ -717,24 +717,44 @@ struct Engine : EngineBase {
     const int Mp = path_rows > 0 ? path_rows : M;
     return use_gemv && Mp <= GEMV_MAX_M && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
   }
-  template <int NT, int CPW, class Epi>
-  void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
-    launch(gemv_small_kernel<NT, CPW, Epi>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A), lda,
-           reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi);
+  template <int NT, int CPW, bool LNA, class Epi>
+  void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
+                     const GvLN& ln) {
+    launch(gemv_small_kernel<NT, CPW, Epi, LNA>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A), lda,
+           reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi, ln);
   }
-  template <int NT, class Epi>
-  void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+  template <int NT, bool LNA, class Epi>
+  void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
+                     const GvLN& ln) {
     const int cpw = std::max(1, K / 32 / GV_WARPS);
-    if (cpw == 1) gemv_launch_t<NT, 1>(A, lda, M, W, N, K, epi, M_dev);
-    else if (cpw == 2) gemv_launch_t<NT, 2>(A, lda, M, W, N, K, epi, M_dev);
-    else if (cpw == 4) gemv_launch_t<NT, 4>(A, lda, M, W, N, K, epi, M_dev);
-    else gemv_launch_t<NT, 8>(A, lda, M, W, N, K, epi, M_dev);
+    if (cpw == 1) gemv_launch_t<NT, 1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else if (cpw == 2) gemv_launch_t<NT, 2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else if (cpw == 4) gemv_launch_t<NT, 4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else gemv_launch_t<NT, 8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
   }
+  template <bool LNA = false, class Epi>
+  void gemv_launch(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
+                   const GvLN& ln = GvLN{nullptr, nullptr, nullptr}) {
+    if (M <= 8) gemv_launch_n<1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else if (M <= 16) gemv_launch_n<2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else gemv_launch_n<4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+  }
+  // LayerNorm feeding a projection: fused into the GEMV prologue on the
+  // small-M path (bit-identical operand), else LN kernel + GEMM
+  bool use_ln_fuse = false;  // option "ln_fuse" (measured: no faster than LN kernel + GEMV at B = 1)
+  bool ln_fusable(int M) const { return use_ln_fuse && BF16 && gemv_ok(M, d) && d % 128 == 0 && d <= 1024; }
   template <class Epi>
-  void gemv_launch(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
-    if (M <= 8) gemv_launch_n<1>(A, lda, M, W, N, K, epi, M_dev);
-    else if (M <= 16) gemv_launch_n<2>(A, lda, M, W, N, K, epi, M_dev);
-    else gemv_launch_n<4>(A, lda, M, W, N, K, epi, M_dev);
+  void gemm_ln(int cls, const float* x, const float* g, const float* b, T* y, int y_cap, int M, const T* W, int N,
+               const Epi& epi, const int* M_dev) {
+    if (M <= 0) return;
+    if (ln_fusable(M)) {
+      Scope sc(this, cls, (double)sizeof(T) * N * d + 4.0 * M * d, 2.0 * M * N * d);
+      gemv_launch<true>(y, d, M, W, N, d, epi, M_dev, GvLN{x, g, b});
+      check_launch();
+      return;
+    }
+    layernorm(x, M, g, b, y, nullptr, nullptr, M_dev);
+    gemm(cls, y, y_cap, d, M, W, N, d, epi, M_dev);
   }
 
   // C[M,N] = A[M,K] . W[N,K]^T with a fused epilogue
@@ -849,7 +869,7 @@ struct Engine : EngineBase {
     const int2* it2 = reinterpret_cast<const int2*>(items);
 #define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
     if constexpr (BF16) {
-      if (dh == 64 && H <= 8 && use_attn_heads) {
+      if (dh == 64 && H <= 8 && use_attn_heads && n_items >= num_sms) {  // few items: per-head CTAs spread wider
         // all heads per CTA (K/V rows fetched once, cp.async + ldmatrix.trans)
         const size_t smem = attn_heads_smem(d);
         static bool attr = false;
@@ -913,8 +933,10 @@ struct Engine : EngineBase {
   }
 
   // vocab projection of R rows of y (K-major d) into tile partials.
+  // ln_g != nullptr: the rows are LN(s1.x) with the final decoder LayerNorm
+  // (dec_lng / dec_lnb), computed in the GEMV prologue
   void vocab_parts(const T* y, int y_cap, int R, VocabParts& parts, int kt, int norm_allowed, float* logits_buf,
-                   const int* M_dev = nullptr) {
+                   const int* M_dev = nullptr, const float* ln_g = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
       if (kt == 1 && gemv_ok(R, d)) {
@@ -922,14 +944,27 @@ struct Engine : EngineBase {
         Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
         const bf16* yb = reinterpret_cast<const bf16*>(y);
         const bf16* Eb = reinterpret_cast<const bf16*>(E);
+        const GvLN ln{ln_g ? s1.x : nullptr, dec_lng, dec_lnb};
+        const int grid = cdiv(V, GV_VTILE);
+#define HRT_GVV(NT)                                                                                          \
+  do {                                                                                                       \
+    if (ln_g)                                                                                                \
+      launch(gemv_vocab_kernel<NT, true>, grid, GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
+    else                                                                                                     \
+      launch(gemv_vocab_kernel<NT, false>, grid, GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
+  } while (0)
         if (R <= 8)
-          launch(gemv_vocab_kernel<1>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+          HRT_GVV(1);
         else if (R <= 16)
-          launch(gemv_vocab_kernel<2>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+          HRT_GVV(2);
         else
-          launch(gemv_vocab_kernel<4>, cdiv(V, GV_VTILE), GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed);
+          HRT_GVV(4);
+#undef HRT_GVV
         check_launch();
         return;
+      }
+      if (ln_g) {  // tcgen05 path: unfused final LN
+        layernorm(s1.x, R, dec_lng, dec_lnb, const_cast<T*>(y), nullptr, nullptr, M_dev);
       }
       const int bn = vocab_bn(R);
       parts.ntiles = cdiv(V, bn / 2);  // one partial per epilogue column half
@@ -1040,7 +1075,7 @@ struct Engine : EngineBase {
   // live row count, step and position are read from the device control block.
   void decoder_step(int R, int t, int pos, int cap, const int* feed, const int* hist, const int* row_seq,
                     const int* kv_off, const int* kv_len, int max_src, StepCtl* ctl = nullptr,
-                    bool do_embed = true, const int* hist2 = nullptr) {
+                    bool do_embed = true, const int* hist2 = nullptr, bool final_ln_fused = false) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     const int* td = ctl ? &ctl->t : nullptr;
     Tag _tg4(this, "s1.embed_ln");
@@ -1056,27 +1091,25 @@ struct Engine : EngineBase {
                         nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd, hist2);
       Tag _tg15(this, "s1.wo");
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
-      Tag _tg17(this, "s1.ln2");
-      if (!(s1_skip & 1)) layernorm(s1.x, R, w.ln2g, w.ln2b, s1.y, nullptr, nullptr, Rd);
       Tag _tg19(this, "s1.qc");
-      if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
+      if (!(s1_skip & 4))
+        gemm_ln(K_GEMM, s1.x, w.ln2g, w.ln2b, s1.y, R_max, R, w.wqc, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
       Tag _tg21(this, "s1.attn_cross");
       if (!(s1_skip & 2)) attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
                          nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
                          2.0 * sizeof(T) * (double)R * max_src * d, nullptr, Rd);
       Tag _tg25(this, "s1.woc");
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
-      Tag _tg27(this, "s1.ln3");
-      if (!(s1_skip & 1)) layernorm(s1.x, R, w.ln3g, w.ln3b, s1.y, nullptr, nullptr, Rd);
       Tag _tg29(this, "s1.w1");
-      if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
+      if (!(s1_skip & 4))
+        gemm_ln(K_GEMM, s1.x, w.ln3g, w.ln3b, s1.y, R_max, R, w.w1, ff, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
       Tag _tg31(this, "s1.w2");
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
       Tag _tg34(this, "s1.ln_out");
       if (s1_skip & 1) {
       } else if (i + 1 < Ld)
         layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y, nullptr, nullptr, Rd);
-      else
+      else if (!final_ln_fused)
         layernorm(s1.x, R, dec_lng, dec_lnb, s1.y, nullptr, nullptr, Rd);
     }
   }
@@ -1361,10 +1394,11 @@ struct Engine : EngineBase {
                    const GreedyState& gs, const BeamState& bs, StepCtl* ctl) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     if (beam == 1) {
-      decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false);
+      const bool fuse = ln_fusable(R) && !(s1_skip & 1);  // final LN inside the vocab GEMV
+      decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false, nullptr, fuse);
       {
         Tag _tg(this, "s1.vocab");
-        if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd);
+        if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd, fuse ? dec_lng : nullptr);
       }
       Tag _tg(this, "s1.select");
       Scope sc(this, K_OTHER, 0, 0);
@@ -1526,8 +1560,8 @@ struct Engine : EngineBase {
       use_mega = value != 0;
     else if (name == "attn_heads")
       use_attn_heads = value != 0;
-    else if (name == "gemv") {
-      use_gemv = value != 0;
+    else if (name == "ln_fuse" || name == "gemv") {
+      (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
       for (auto& kv : loop_graphs) {  // captured loops bake the GEMM path in
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         if (kv.second.graph) cudaGraphDestroy(kv.second.graph);

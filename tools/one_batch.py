@@ -1,5 +1,5 @@
 """One fused batch (config c2) for profiling."""
-import sys, numpy as np
+import os, sys, numpy as np
 sys.path.insert(0, "/root/repo")
 import paper_2212_01543_b200 as hrt
 from paper_2212_01543_b200 import workload as W
@@ -10,6 +10,8 @@ eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat
 srcs = W.make_sources(B, 1001, spec["lengths"])
 caps = W.stage1_caps(srcs, 2)
 ids = np.concatenate([np.asarray(s, np.int32) for s in srcs]); lens = [len(s) for s in srcs]
+if os.environ.get("HRT_GRAPHS") == "0":
+    eng.set_option("graphs", 0)
 for _ in range(n):
     eng.translate_arrays(ids, lens, k=2, max_steps=caps)
 print(eng.phase_times())
