@@ -140,6 +140,20 @@ def peaks():
     return 6650.0, 1400.0, 1590.0, "fallback"
 
 
+def profiled_traffic(g):
+    """DRAM bytes per GEMM launch from the committed ncu capture of this
+    workload (profiles/*gemm_traffic*.json, written by tools/ncu_summary.py),
+    or None when no capture is present."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "*gemm_traffic*.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        j = json.load(f)
+    return j.get("gemm_dram_bytes_per_launch"), os.path.relpath(files[-1], REPO)
+
+
 # ---------------------------------------------------------------------------
 # CPU reference (oracle port of the reference's CPU path)
 # ---------------------------------------------------------------------------
@@ -431,9 +445,11 @@ def run_engine(args):
         return
     hbm, tf_sus, tf_burst, src = peaks()
     gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    traffic, traffic_src = profiled_traffic(g)
     roof = {"bound": "tensor", "kernel": "tcgen05 GEMMs (all projections + vocab, one step)",
             "achieved": gemm_tflops, "peak": tf_sus, "unit": "TFLOP/s",
-            "frac": (gemm_tflops / tf_sus) if gemm_tflops else None, "traffic": None,
+            "frac": (gemm_tflops / tf_sus) if gemm_tflops else None, "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
             "gemm_ms_per_step": g["ms"], "gemm_launches_per_step": g["launches"],
             "gemm_share_of_step": g["ms"] / ms_all if ms_all else None,
@@ -453,7 +469,7 @@ def run_engine(args):
                    "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e_tot / args.steps},
-        "gpu_launches": launches // max(1, args.steps),
+        "gpu_launches": launches, "gpu_launches_per_step": launches // max(1, args.steps),
         "phase_ms_per_step": phase_ms, "stage1_steps_per_step": stage1_steps,
         "roofline": roof,
         "cpu_baseline": None if cpu is None else {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},

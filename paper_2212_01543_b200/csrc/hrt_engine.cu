@@ -212,7 +212,7 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
-  bool use_attn_heads = true;  // option "attn_heads": all-heads-per-CTA prefill attention
+  int attn_heads_mode = 1;  // option "attn_heads": all-heads-per-CTA prefill attention (0 off, 1 auto, 2 always)
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
   float4* mg_vpart = nullptr;
@@ -869,8 +869,8 @@ struct Engine : EngineBase {
     const int2* it2 = reinterpret_cast<const int2*>(items);
 #define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
     if constexpr (BF16) {
-      if (dh == 64 && H <= 8 && use_attn_heads && n_items >= num_sms) {  // few items: per-head CTAs spread wider
-        // all heads per CTA (K/V rows fetched once, cp.async + ldmatrix.trans)
+      // all heads per CTA (K/V rows fetched once); with few work items per-head CTAs spread wider
+      if (dh == 64 && H <= 8 && (attn_heads_mode == 2 || (attn_heads_mode == 1 && n_items >= num_sms))) {
         const size_t smem = attn_heads_smem(d);
         static bool attr = false;
         if (!attr) {
@@ -1559,7 +1559,7 @@ struct Engine : EngineBase {
     else if (name == "mega")
       use_mega = value != 0;
     else if (name == "attn_heads")
-      use_attn_heads = value != 0;
+      attn_heads_mode = value;
     else if (name == "ln_fuse" || name == "gemv") {
       (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
       for (auto& kv : loop_graphs) {  // captured loops bake the GEMM path in

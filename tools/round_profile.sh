@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round-end measurement + profiling pass (run under gpurun from the repo root).
+#   tools/round_profile.sh <tag>
+set -u
+TAG=${1:-r1}
+OUT=gpurun_out
+mkdir -p $OUT
+timeout 900 python -m pytest tests -m gpu -q > $OUT/${TAG}_pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1
+timeout 600 python bench.py > $OUT/${TAG}_bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/${TAG}_bench_ref.log 2>&1
+# launch lists (eager: kernels inside conditional-node graphs cannot be profiled individually)
+for B in 1024 1; do
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --profile-from-start off --csv --log-file $OUT/${TAG}_launches_c2_b$B.csv \
+    python tools/profile_step.py --batch $B --no-graph > $OUT/${TAG}_ncu_list_b$B.log 2>&1
+done
+# one full capture of the top kernel class (encoder QKV/W1 GEMM at B=1024)
+timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
+  -k regex:tc_gemm_kernel -s 2 -c 1 -o $OUT/${TAG}_gemm_full \
+  python tools/profile_step.py --batch 1024 --no-graph > $OUT/${TAG}_ncu_full.log 2>&1
+echo done
