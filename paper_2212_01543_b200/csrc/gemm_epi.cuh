@@ -67,6 +67,13 @@ struct EpiBiasT {
     if (RELU) a = fmaxf(a, 0.f);
     out[(size_t)row * ldo + col] = from_f<T>(a);
   }
+  // split form for latency-bound callers: every operand load issued before any store
+  __device__ __forceinline__ float2 load2(int, int col) const { return make_float2(__ldg(bias + col), 0.f); }
+  __device__ __forceinline__ void store2(int row, int col, float v, float2 pre) const {
+    float a = v + pre.x;
+    if (RELU) a = fmaxf(a, 0.f);
+    out[(size_t)row * ldo + col] = from_f<T>(a);
+  }
 };
 
 struct EpiResidual {
@@ -106,6 +113,12 @@ struct EpiResidual {
   __device__ __forceinline__ void apply1(int row, int col, float v) const {
     x[(size_t)row * ldx + col] += v + bias[col];
   }
+  __device__ __forceinline__ float2 load2(int row, int col) const {
+    return make_float2(x[(size_t)row * ldx + col], __ldg(bias + col));
+  }
+  __device__ __forceinline__ void store2(int row, int col, float v, float2 pre) const {
+    x[(size_t)row * ldx + col] = pre.x + (v + pre.y);
+  }
 };
 
 struct EpiStoreF32 {
@@ -122,6 +135,8 @@ struct EpiStoreF32 {
       if (row0 + 4 * i < M) store4(out + (size_t)(row0 + 4 * i) * ldo + col, v[i]);
   }
   __device__ __forceinline__ void apply1(int row, int col, float v) const { out[(size_t)row * ldo + col] = v; }
+  __device__ __forceinline__ float2 load2(int, int) const { return make_float2(0.f, 0.f); }
+  __device__ __forceinline__ void store2(int row, int col, float v, float2) const { out[(size_t)row * ldo + col] = v; }
 };
 
 }  // namespace hrt

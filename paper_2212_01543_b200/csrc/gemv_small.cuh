@@ -139,6 +139,21 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
+  // epilogue operands (residual rows, bias) of the outputs warp 0 owns: issued now, consumed after the reduction
+  const int f0 = n0 + g, f1 = f0 + 8;
+  float2 pre[NT][4];
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int r0 = 8 * j + 2 * t4;
+      const int ra = min(r0, M - 1), rb = min(r0 + 1, M - 1);
+      const int fa = min(f0, N - 1), fb = min(f1, N - 1);
+      pre[j][0] = epi.load2(ra, fa);
+      pre[j][1] = epi.load2(rb, fa);
+      pre[j][2] = epi.load2(ra, fb);
+      pre[j][3] = epi.load2(rb, fb);
+    }
+  }
   if (LNA) {
     gv_ln_stats(ln, M, K, lnst);
     __syncthreads();
@@ -180,17 +195,16 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
     }
   }
   if (warp != 0) return;
-  const int f0 = n0 + g, f1 = f0 + 8;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const int r0 = 8 * j + 2 * t4;
     if (r0 < M) {
-      if (f0 < N) epi.apply1(r0, f0, c[j][0]);
-      if (f1 < N) epi.apply1(r0, f1, c[j][2]);
+      if (f0 < N) epi.store2(r0, f0, c[j][0], pre[j][0]);
+      if (f1 < N) epi.store2(r0, f1, c[j][2], pre[j][2]);
     }
     if (r0 + 1 < M) {
-      if (f0 < N) epi.apply1(r0 + 1, f0, c[j][1]);
-      if (f1 < N) epi.apply1(r0 + 1, f1, c[j][3]);
+      if (f0 < N) epi.store2(r0 + 1, f0, c[j][1], pre[j][1]);
+      if (f1 < N) epi.store2(r0 + 1, f1, c[j][3], pre[j][3]);
     }
   }
 }

@@ -708,14 +708,19 @@ struct Engine : EngineBase {
   // small-M regime (decode steps at small batch, batch-1 encoder / Stage II):
   // mma.sync GEMV with K split over the warps of a CTA (gemv_small.cuh)
   bool use_gemv = true;  // option "gemv"
-  static constexpr int GEMV_MAX_M = 32;
+  int gemv_max_m = 32;  // option "gemv_max_m" (32 or 64)
   // path_rows: when set (eager Stage-I loop), the kernel choice follows the
   // captured graph's row bucket instead of the live row count, so eager and
   // graph launches run the same kernels (bit-identical results)
   int path_rows = 0;
   bool gemv_ok(int M, int K) const {
     const int Mp = path_rows > 0 ? path_rows : M;
-    return use_gemv && Mp <= GEMV_MAX_M && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
+    return use_gemv && Mp <= gemv_max_m && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
+  }
+  // the vocabulary GEMV keeps per-row statistics in registers: at most 32 rows
+  bool gemv_vocab_ok(int M) const {
+    const int Mp = path_rows > 0 ? path_rows : M;
+    return gemv_ok(M, d) && Mp <= 32;
   }
   template <int NT, int CPW, bool LNA, class Epi>
   void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
@@ -737,12 +742,13 @@ struct Engine : EngineBase {
                    const GvLN& ln = GvLN{nullptr, nullptr, nullptr}) {
     if (M <= 8) gemv_launch_n<1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
     else if (M <= 16) gemv_launch_n<2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else gemv_launch_n<4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else if (M <= 32) gemv_launch_n<4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else gemv_launch_n<8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
   }
   // LayerNorm feeding a projection: fused into the GEMV prologue on the
   // small-M path (bit-identical operand), else LN kernel + GEMM
   bool use_ln_fuse = false;  // option "ln_fuse" (measured: no faster than LN kernel + GEMV at B = 1)
-  bool ln_fusable(int M) const { return use_ln_fuse && BF16 && gemv_ok(M, d) && d % 128 == 0 && d <= 1024; }
+  bool ln_fusable(int M) const { return use_ln_fuse && BF16 && gemv_vocab_ok(M) && d % 128 == 0 && d <= 1024; }
   template <class Epi>
   void gemm_ln(int cls, const float* x, const float* g, const float* b, T* y, int y_cap, int M, const T* W, int N,
                const Epi& epi, const int* M_dev) {
@@ -939,7 +945,7 @@ struct Engine : EngineBase {
                    const int* M_dev = nullptr, const float* ln_g = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
-      if (kt == 1 && gemv_ok(R, d)) {
+      if (kt == 1 && gemv_vocab_ok(R)) {
         parts.ntiles = cdiv(V, GV_VTILE);
         Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
         const bf16* yb = reinterpret_cast<const bf16*>(y);
@@ -1560,8 +1566,13 @@ struct Engine : EngineBase {
       use_mega = value != 0;
     else if (name == "attn_heads")
       attn_heads_mode = value;
-    else if (name == "ln_fuse" || name == "gemv") {
-      (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
+    else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
+      if (name == "gemv_max_m") {
+        if (value != 32 && value != 64) throw HrtError(HRT_ERR_INVALID, "gemv_max_m must be 32 or 64");
+        gemv_max_m = value;
+      } else {
+        (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
+      }
       for (auto& kv : loop_graphs) {  // captured loops bake the GEMM path in
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
