@@ -213,6 +213,8 @@ struct Engine : EngineBase {
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
   int attn_heads_mode = 1;  // option "attn_heads": all-heads-per-CTA prefill attention (0 off, 1 auto, 2 always)
+  bool use_attn_rows = true;  // option "attn_rows": CTA-per-row decode attention
+  bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
   float4* mg_vpart = nullptr;
@@ -922,6 +924,29 @@ struct Engine : EngineBase {
                    double bytes, const int* t_dev = nullptr, const int* R_dev = nullptr, const int* hist2 = nullptr) {
     if (R <= 0) return;
     Scope sc(this, K_ATTN, bytes, 0.0);
+    if constexpr (BF16) {
+      // large row counts only (few rows: the warp-per-(row, head) kernel spreads wider); the
+      // choice follows the graph's row bucket so graph and eager runs match bit for bit
+      const int Rp = path_rows > 0 ? path_rows : R;
+      if (dh == 64 && H <= 16 && use_attn_rows && Rp >= 256) {
+        // one CTA per row, all heads: coalesced whole-row K/V staging
+        const size_t smem = attn_rows_smem(d);
+        static bool attr = false;
+        if (!attr) {
+          CUDA_OK(cudaFuncSetAttribute(attn_decode_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn_rows_smem(1024)));
+          CUDA_OK(cudaFuncSetAttribute(attn_decode_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn_rows_smem(1024)));
+          attr = true;
+        }
+        const int threads = std::max(64, H * 32);
+        launch(attn_decode_rows_kernel<SELF>, R, threads, smem, q, qs, kn, vn, ns, kc, vc, d,
+               greedy_hist_identity ? nullptr : hist, greedy_hist_identity ? nullptr : hist2, cap, t, t_dev, row_seq,
+               kv_off, kv_len, R_dev, R, H, att_scale, out, d);
+        check_launch();
+        return;
+      }
+    }
     const int nwarp = 4;
     lk_max = std::max(lk_max, 1);
     const size_t smem = (size_t)nwarp * lk_max * sizeof(float);
@@ -1401,7 +1426,15 @@ struct Engine : EngineBase {
     const int* Rd = ctl ? &ctl->R : nullptr;
     if (beam == 1) {
       const bool fuse = ln_fusable(R) && !(s1_skip & 1);  // final LN inside the vocab GEMV
-      decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false, nullptr, fuse);
+      greedy_hist_identity = true;  // greedy rows never reorder: slot j of row r is row r
+      try {
+        decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false, nullptr,
+                     fuse);
+      } catch (...) {
+        greedy_hist_identity = false;
+        throw;
+      }
+      greedy_hist_identity = false;
       {
         Tag _tg(this, "s1.vocab");
         if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd, fuse ? dec_lng : nullptr);
@@ -1566,6 +1599,14 @@ struct Engine : EngineBase {
       use_mega = value != 0;
     else if (name == "attn_heads")
       attn_heads_mode = value;
+    else if (name == "attn_rows") {
+      use_attn_rows = value != 0;
+      for (auto& kv : loop_graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      }
+      loop_graphs.clear();
+    }
     else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
       if (name == "gemv_max_m") {
         if (value != 32 && value != 64) throw HrtError(HRT_ERR_INVALID, "gemv_max_m must be 32 or 64");

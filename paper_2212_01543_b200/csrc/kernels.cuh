@@ -687,6 +687,139 @@ __global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Decode attention, one CTA per Stage-I row covering every head (bf16,
+// d_head = 64, heads <= 16): the row's key/value rows (all heads, d wide and
+// contiguous) are staged through shared memory in 32-key chunks with
+// cp.async, so each key row is one coalesced d*2-byte transfer instead of
+// per-head strided reads; warp h then runs head h with one key per lane for
+// QK^T and two head dims per lane for PV (online softmax across chunks).
+// SELF: appends this step's k/v at cache slot t (history slot j of logical row
+// r lives in physical row hist[r * cap + j], or row r when hist == nullptr).
+// CROSS: attends the row's sentence memory keys (computed once in encode).
+// Same arguments and results as attn_decode_kernel (infer.py:259-285).
+// ---------------------------------------------------------------------------
+constexpr int AD_KC = 32, AD_PAD = 8;
+
+inline size_t attn_rows_smem(int d) {
+  return (size_t)2 * AD_KC * (d + AD_PAD) * 2 + (size_t)d * sizeof(float) + AD_KC * sizeof(int);
+}
+
+template <bool SELF>
+__global__ void __launch_bounds__(512) attn_decode_rows_kernel(
+    const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ knew, const bf16* __restrict__ vnew,
+    int new_stride, bf16* __restrict__ kc, bf16* __restrict__ vc, int c_stride, const int* __restrict__ hist_a,
+    const int* __restrict__ hist_b, int cap, int t, const int* __restrict__ t_dev, const int* __restrict__ row_seq,
+    const int* __restrict__ kv_off, const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads,
+    float scale, bf16* __restrict__ out, int out_stride) {
+  pdl_enter();
+  constexpr int DH = 64;
+  extern __shared__ __align__(16) unsigned char ad_raw[];
+  if (R_dev) R = *R_dev;
+  if (t_dev) t = *t_dev;
+  const int r = blockIdx.x;
+  if (r >= R) return;
+  const int d = heads * DH, ld = d + AD_PAD, c8n = d / 8;
+  bf16* Ks = reinterpret_cast<bf16*>(ad_raw);
+  bf16* Vs = Ks + AD_KC * ld;
+  float* qs = reinterpret_cast<float*>(Vs + AD_KC * ld);
+  int* hs = reinterpret_cast<int*>(qs + d);
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
+  int L;
+  size_t kv_row0 = 0;
+  if (SELF) {
+    L = t + 1;
+    // append this step's k / v at slot t (all heads)
+    const size_t dst = ((size_t)r * cap + t) * c_stride;
+    for (int c = tid; c < c8n; c += nthr) {
+      *reinterpret_cast<uint4*>(kc + dst + c * 8) = *reinterpret_cast<const uint4*>(knew + (size_t)r * new_stride + c * 8);
+      *reinterpret_cast<uint4*>(vc + dst + c * 8) = *reinterpret_cast<const uint4*>(vnew + (size_t)r * new_stride + c * 8);
+    }
+  } else {
+    const int sq = row_seq ? row_seq[r] : r;
+    L = kv_len[sq];
+    kv_row0 = kv_off[sq];
+  }
+  for (int c = tid; c < d; c += nthr) qs[c] = to_f(q[(size_t)r * q_stride + c]) * scale;
+  const int h = warp;
+  const bool active = h < heads;
+  float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f;
+  for (int j0 = 0; j0 < L; j0 += AD_KC) {
+    const int nk = min(AD_KC, L - j0);
+    __syncthreads();  // previous chunk consumed (and qs / the cache append visible)
+    if (SELF && hist) {
+      for (int j = tid; j < nk; j += nthr) hs[j] = hist[(size_t)r * cap + j0 + j];
+      __syncthreads();
+    }
+    for (int idx = tid; idx < nk * c8n; idx += nthr) {
+      const int j = idx / c8n, c = (idx - j * c8n) * 8;
+      const bf16* ksrc;
+      const bf16* vsrc;
+      if (SELF) {
+        const int jj = j0 + j;
+        if (jj == t) {
+          ksrc = knew + (size_t)r * new_stride + c;
+          vsrc = vnew + (size_t)r * new_stride + c;
+        } else {
+          const size_t pr = ((size_t)(hist ? hs[j] : r) * cap + jj) * c_stride + c;
+          ksrc = kc + pr;
+          vsrc = vc + pr;
+        }
+      } else {
+        const size_t pr = (kv_row0 + j0 + j) * (size_t)new_stride + c;
+        ksrc = knew + pr;
+        vsrc = vnew + pr;
+      }
+      const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(Ks + j * ld + c));
+      const uint32_t sv = static_cast<uint32_t>(__cvta_generic_to_shared(Vs + j * ld + c));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sk), "l"(ksrc) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sv), "l"(vsrc) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (active) {
+      // scores: lane = key of the chunk (same dot order as attn_decode_kernel)
+      float s = -INFINITY;
+      if (lane < nk) {
+        const bf16* kr = Ks + lane * ld + h * DH;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < DH; c += 8) {
+          float kk[8];
+          load8(kr + c, kk);
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            a0 = fmaf(qs[h * DH + c + e], kk[e], a0);
+            a1 = fmaf(qs[h * DH + c + e + 1], kk[e + 1], a1);
+          }
+        }
+        s = a0 + a1;
+      }
+      const float mn = fmaxf(m, warp_max(s));
+      const float sc = ex2f((m - mn) * LOG2E);  // first chunk: m = -inf -> 0
+      const float p = lane < nk ? ex2f((s - mn) * LOG2E) : 0.f;
+      l = l * sc + warp_sum(p);
+      m = mn;
+      o0 *= sc;
+      o1 *= sc;
+      const bf16* vcol = Vs + h * DH + 2 * lane;
+      for (int i = 0; i < nk; ++i) {
+        const float pi = __shfl_sync(0xffffffffu, p, i);
+        const float2 v2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vcol + i * ld));
+        o0 = fmaf(pi, v2.x, o0);
+        o1 = fmaf(pi, v2.y, o1);
+      }
+    }
+  }
+  if (active) {
+    const float inv = 1.0f / l;
+    *reinterpret_cast<__nv_bfloat162*>(out + (size_t)r * out_stride + h * DH + 2 * lane) =
+        __floats2bfloat162_rn(o0 * inv, o1 * inv);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Single-query attention for one Stage-I decoder step (infer.py:259-285).
 // SELF: append this step's k/v at cache slot t, then attend slots 0..t of the
 //       row's history; history slot j of logical row r lives in physical row
