@@ -213,7 +213,7 @@ struct Engine : EngineBase {
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
   int attn_heads_mode = 1;  // option "attn_heads": all-heads-per-CTA prefill attention (0 off, 1 auto, 2 always)
-  bool use_attn_rows = true;  // option "attn_rows": CTA-per-row decode attention
+  int attn_rows_mode = 1;  // option "attn_rows": CTA-per-row decode attention (0 off, 1 >= 256 rows, 2 always)
   bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
@@ -928,7 +928,7 @@ struct Engine : EngineBase {
       // large row counts only (few rows: the warp-per-(row, head) kernel spreads wider); the
       // choice follows the graph's row bucket so graph and eager runs match bit for bit
       const int Rp = path_rows > 0 ? path_rows : R;
-      if (dh == 64 && H <= 16 && use_attn_rows && Rp >= 256) {
+      if (dh == 64 && H <= 16 && (attn_rows_mode == 2 || (attn_rows_mode == 1 && Rp >= 256))) {
         // one CTA per row, all heads: coalesced whole-row K/V staging
         const size_t smem = attn_rows_smem(d);
         static bool attr = false;
@@ -1600,7 +1600,7 @@ struct Engine : EngineBase {
     else if (name == "attn_heads")
       attn_heads_mode = value;
     else if (name == "attn_rows") {
-      use_attn_rows = value != 0;
+      attn_rows_mode = value;
       for (auto& kv : loop_graphs) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         if (kv.second.graph) cudaGraphDestroy(kv.second.graph);

@@ -418,3 +418,21 @@ def test_small_batch_gemv_paths_match_and_fused_ln_is_exact(hrt):
         tot += max(len(a.tokens), len(b.tokens))
         agree += sum(x == y for x, y in zip(a.tokens, b.tokens))
     assert agree / tot > 0.95
+
+
+def test_decode_attention_row_kernel_matches_head_kernel(hrt, golden):
+    """CTA-per-row decode attention (all heads, staged K/V) vs the
+    warp-per-(row, head) kernel, greedy and beam (history map in use)."""
+    g = golden("dh64")
+    eng = hrt.Engine(_model(hrt, g), dtype="bfloat16", max_sentences=8, max_beam=4)
+    srcs = g["sources"]
+    for b_at, b_nat in ((1, 1), (4, 2)):
+        res = {}
+        for mode in (2, 0):
+            eng.set_option("attn_rows", mode)
+            res[mode] = eng.translate_batch(srcs, 2, b_at, b_nat)
+        eng.set_option("attn_rows", 1)
+        agree = sum(a.tokens == b.tokens for a, b in zip(res[2], res[0]))
+        assert agree >= len(srcs) - 1, (b_at, agree)
+        for a, b in zip(res[2], res[0]):
+            assert a.decoder_calls == b.decoder_calls
