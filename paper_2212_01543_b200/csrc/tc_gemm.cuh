@@ -23,6 +23,7 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
 constexpr int TC_EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half the tile columns
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+constexpr int TC_STG_LD = 32;  // epilogue transpose row pitch (floats); 16-byte slots XOR-swizzled by row
 
 template <int BN, int STAGES>
 struct TcSmem {
@@ -30,7 +31,7 @@ struct TcSmem {
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFFSET = STAGES * STAGE_BYTES;                // epilogue staging
-  static constexpr int STG_BYTES = TC_EPI_WARPS * 32 * 33 * 4;
+  static constexpr int STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
   static constexpr int BAR_OFFSET = STG_OFFSET + STG_BYTES;
   static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;  // barriers + alignment slack
 };
@@ -57,6 +58,16 @@ struct SplitK {
   int splits;
   float* ws;
   int* counters;
+};
+
+// element-wise epilogues that store whole per-lane row segments (Epi::kRowStore)
+template <class E, class = void>
+struct EpiRowStore {
+  static constexpr bool value = false;
+};
+template <class E>
+struct EpiRowStore<E, decltype(void(E::kRowStore))> {
+  static constexpr bool value = E::kRowStore;
 };
 
 template <int BN, int STAGES, class Epi>
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int cbeg = (ew / 4) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
-    float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * 33);
+    float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * TC_STG_LD);
     int it = 0;
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
@@ -212,21 +223,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
         }
         if (live) epi.end(st, row, n0 + cbeg);
+      } else if constexpr (EpiRowStore<Epi>::value) {
+        // lane = row: the lane's 32 consecutive columns go out as full 64 / 128-byte
+        // row segments (no shared-memory transpose)
+        const int row = rbase + lane;
+#pragma unroll 1
+        for (int c = cbeg; c < cend; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          const int col0 = n0 + c;
+          if (row < M && col0 < N) epi.row32(row, col0, v, N - col0);
+        }
       } else {
         const int Mpad = m_tiles * TC_BM;
+        // each 32-column chunk is transposed through shared memory with
+        // 16-byte accesses so global traffic is coalesced row segments
 #pragma unroll 1
         for (int c = cbeg; c < cend; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+          for (int i = 0; i < 8; ++i)  // row `lane`, slot i -> physical slot i ^ (row & 7): conflict-free
+            *reinterpret_cast<float4*>(stg + lane * TC_STG_LD + 4 * (i ^ (lane & 7))) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           __syncwarp();
           const int col = n0 + c + (lane & 7) * 4;
           float4 vals[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float* s = stg + (i * 4 + (lane >> 3)) * 33 + (lane & 7) * 4;
-            vals[i] = make_float4(s[0], s[1], s[2], s[3]);
+            const int r = i * 4 + (lane >> 3);
+            vals[i] = *reinterpret_cast<const float4*>(stg + r * TC_STG_LD + 4 * ((lane & 7) ^ (r & 7)));
           }
           if (S == 1) {
             // rows rbase + (lane >> 3) + 4 i; all global loads of the group are
