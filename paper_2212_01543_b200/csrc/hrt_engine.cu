@@ -878,16 +878,26 @@ struct Engine : EngineBase {
 #define HRT_PF(DHV) prefill_launch<DHV>(grid, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal)
     if constexpr (BF16) {
       // all heads per CTA (K/V rows fetched once); with few work items per-head CTAs spread wider
-      if (dh == 64 && H <= 8 && (attn_heads_mode == 2 || (attn_heads_mode == 1 && n_items >= num_sms))) {
+      if (dh == 64 && (H == 1 || H == 2 || H == 4 || H == 8) &&
+          (attn_heads_mode == 2 || (attn_heads_mode == 1 && n_items >= num_sms))) {
         const size_t smem = attn_heads_smem(d);
-        static bool attr = false;
-        if (!attr) {
-          CUDA_OK(cudaFuncSetAttribute(attn_prefill_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)attn_heads_smem(512)));
-          attr = true;
-        }
-        launch(attn_prefill_heads_kernel, dim3(n_items), 2 * H * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off,
-               q_slot, q_len, kv_map, kv_off, kv_len, key_ok, causal, att_scale, H);
+        auto go = [&](auto kern) {
+          static bool attr = false;
+          if (!attr) {
+            CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_heads_smem(512)));
+            attr = true;
+          }
+          launch(kern, dim3(n_items), 2 * H * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map,
+                 kv_off, kv_len, key_ok, causal, att_scale, H);
+        };
+        if (H == 8)
+          go(attn_prefill_heads_kernel<8>);
+        else if (H == 4)
+          go(attn_prefill_heads_kernel<4>);
+        else if (H == 2)
+          go(attn_prefill_heads_kernel<2>);
+        else
+          go(attn_prefill_heads_kernel<1>);
         check_launch();
         return;
       }

@@ -521,6 +521,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 
 inline size_t attn_heads_smem(int d) { return (size_t)(32 + 2 * AH_KC) * (d + AH_PAD) * 2 + AH_KC * sizeof(float); }
 
+template <int HT>  // heads (compile-time: index math by shifts)
 __global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
     const int2* __restrict__ items, const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ k,
     const bf16* __restrict__ v, int kv_stride, bf16* __restrict__ out, int out_stride, const int* __restrict__ q_off,
@@ -530,7 +531,8 @@ __global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
   pdl_enter();
   constexpr int DH = 64;
   extern __shared__ __align__(16) unsigned char ah_raw[];
-  const int d = H * DH, ld = d + AH_PAD, c8n = d / 8;
+  (void)H;
+  constexpr int d = HT * DH, ld = d + AH_PAD, c8n = d / 8;
   bf16* Qs = reinterpret_cast<bf16*>(ah_raw);
   bf16* Ks = Qs + 32 * ld;
   bf16* Vs = Ks + AH_KC * ld;
