@@ -139,19 +139,24 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
-  // epilogue operands (residual rows, bias) of the outputs warp 0 owns: issued now, consumed after the reduction
+  // The final reduction and epilogue are spread over NG warps: warp w < NG owns
+  // n-tiles w, w + NG, ...; its epilogue operands (residual rows, bias) are
+  // issued now and consumed after the reduction.
+  constexpr int NOWN = NT / NG;
+  const bool owner = warp < NG;
   const int f0 = n0 + g, f1 = f0 + 8;
-  float2 pre[NT][4];
-  if (warp == 0) {
+  float2 pre[NOWN][4];
+  if (owner) {
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+    for (int o = 0; o < NOWN; ++o) {
+      const int j = o * NG + warp;
       const int r0 = 8 * j + 2 * t4;
       const int ra = min(r0, M - 1), rb = min(r0 + 1, M - 1);
       const int fa = min(f0, N - 1), fb = min(f1, N - 1);
-      pre[j][0] = epi.load2(ra, fa);
-      pre[j][1] = epi.load2(rb, fa);
-      pre[j][2] = epi.load2(ra, fb);
-      pre[j][3] = epi.load2(rb, fb);
+      pre[o][0] = epi.load2(ra, fa);
+      pre[o][1] = epi.load2(rb, fa);
+      pre[o][2] = epi.load2(ra, fb);
+      pre[o][3] = epi.load2(rb, fb);
     }
   }
   if (LNA) {
@@ -161,50 +166,53 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   float c[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
-  // activation (B) fragments: row 8j+g, k = 32 ch + 8 t
+  // activation (B) fragments: row 8j+g, k = 32 ch + 8 t (n-tiles past M skipped)
+  const int nt_live = min(NT, (M + 7) / 8);
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     if (c0 + i < c1) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        const int r = min(8 * j + g, M - 1);
-        const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (c0 + i) + t4 * 8);
-        gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
-        gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
+        if (j < nt_live) {
+          const int r = min(8 * j + g, M - 1);
+          const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (c0 + i) + t4 * 8);
+          gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
+          gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
+        }
       }
     }
   }
   // fixed-order reduction over the warps, NG n-tiles per pass
+  float fin[NOWN][4];
 #pragma unroll
-  for (int j0 = 0; j0 < NT; j0 += NG) {
-    if (j0 > 0) __syncthreads();
+  for (int o = 0; o < NOWN; ++o) {
+    if (o > 0) __syncthreads();
 #pragma unroll
     for (int j = 0; j < NG; ++j)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) red[warp][j * 4 + e][lane] = c[j0 + j][e];
+      for (int e = 0; e < 4; ++e) red[warp][j * 4 + e][lane] = c[o * NG + j][e];
     __syncthreads();
-    if (warp == 0) {
+    if (owner) {
 #pragma unroll
-      for (int j = 0; j < NG; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float s = red[0][j * 4 + e][lane];
-          for (int w = 1; w < GV_WARPS; ++w) s += red[w][j * 4 + e][lane];
-          c[j0 + j][e] = s;
-        }
+      for (int e = 0; e < 4; ++e) {
+        float sum = red[0][warp * 4 + e][lane];
+        for (int w = 1; w < GV_WARPS; ++w) sum += red[w][warp * 4 + e][lane];
+        fin[o][e] = sum;
+      }
     }
   }
-  if (warp != 0) return;
+  if (!owner) return;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
+  for (int o = 0; o < NOWN; ++o) {
+    const int j = o * NG + warp;
     const int r0 = 8 * j + 2 * t4;
     if (r0 < M) {
-      if (f0 < N) epi.store2(r0, f0, c[j][0], pre[j][0]);
-      if (f1 < N) epi.store2(r0, f1, c[j][2], pre[j][2]);
+      if (f0 < N) epi.store2(r0, f0, fin[o][0], pre[o][0]);
+      if (f1 < N) epi.store2(r0, f1, fin[o][2], pre[o][2]);
     }
     if (r0 + 1 < M) {
-      if (f0 < N) epi.store2(r0 + 1, f0, c[j][1], pre[j][1]);
-      if (f1 < N) epi.store2(r0 + 1, f1, c[j][3], pre[j][3]);
+      if (f0 < N) epi.store2(r0 + 1, f0, fin[o][1], pre[o][1]);
+      if (f1 < N) epi.store2(r0 + 1, f1, fin[o][3], pre[o][3]);
     }
   }
 }

@@ -710,7 +710,7 @@ struct Engine : EngineBase {
   // small-M regime (decode steps at small batch, batch-1 encoder / Stage II):
   // mma.sync GEMV with K split over the warps of a CTA (gemv_small.cuh)
   bool use_gemv = true;  // option "gemv"
-  int gemv_max_m = 32;  // option "gemv_max_m" (32 or 64)
+  int gemv_max_m = 64;  // option "gemv_max_m" (32, 64 or 128; measured best: 64)
   // path_rows: when set (eager Stage-I loop), the kernel choice follows the
   // captured graph's row bucket instead of the live row count, so eager and
   // graph launches run the same kernels (bit-identical results)
@@ -745,7 +745,8 @@ struct Engine : EngineBase {
     if (M <= 8) gemv_launch_n<1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
     else if (M <= 16) gemv_launch_n<2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
     else if (M <= 32) gemv_launch_n<4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else gemv_launch_n<8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else if (M <= 64) gemv_launch_n<8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    else gemv_launch_n<16, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
   }
   // LayerNorm feeding a projection: fused into the GEMV prologue on the
   // small-M path (bit-identical operand), else LN kernel + GEMM
@@ -1600,11 +1601,20 @@ struct Engine : EngineBase {
     CUDA_OK(cudaMemcpy(out, mg_trace, std::min(n, 64) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
 
+  void drop_loop_graphs() {  // options that change kernel choice invalidate the captured loops
+    for (auto& kv : loop_graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
+    loop_graphs.clear();
+  }
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
-    else if (name == "splitk")
+    else if (name == "splitk") {
       use_splitk = value != 0;
+      drop_loop_graphs();
+    }
     else if (name == "mega")
       use_mega = value != 0;
     else if (name == "attn_heads")
@@ -1619,7 +1629,7 @@ struct Engine : EngineBase {
     }
     else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
       if (name == "gemv_max_m") {
-        if (value != 32 && value != 64) throw HrtError(HRT_ERR_INVALID, "gemv_max_m must be 32 or 64");
+        if (value != 32 && value != 64 && value != 128) throw HrtError(HRT_ERR_INVALID, "gemv_max_m: 32, 64 or 128");
         gemv_max_m = value;
       } else {
         (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
