@@ -513,7 +513,7 @@ struct Engine : EngineBase {
 
   // vocab GEMM tile width: 256 whenever the vocabulary is large (fewer
   // partials per row for the selection merge, one tile per CTA at small R)
-  int vocab_bn(int rows) const { return V >= 4096 ? 256 : choose_bn(rows, V); }
+  int vocab_bn(int rows) const { return V >= 4096 ? 256 : std::max(64, choose_bn(rows, V)); }  // row-wise epilogue: column halves
   // upper bound on vocab tiles per row for any row count (partials sizing)
   int nt_bound() const { return (BF16 && V < 4096) ? cdiv(V, 32) : cdiv(V, 128); }
 
@@ -699,11 +699,13 @@ struct Engine : EngineBase {
 
   // widest N tile that still fills ~0.6 of the SMs (large-M encoder / Stage-II
   // GEMMs -> 256, Stage-I GEMMs with few row tiles -> 128 or 64)
+  int bn32_mode = 1;  // option "bn32": 32-column tiles when 64-column tiles leave most SMs idle
   int choose_bn(int M, int N) const {
-    if (M <= 128) return 64;
     const int mt = cdiv(M, TC_BM);
-    for (int bn : {256, 128})
-      if (mt * cdiv(N, bn) * 10 >= num_sms * 6) return bn;
+    if (M > 128)
+      for (int bn : {256, 128})
+        if (mt * cdiv(N, bn) * 10 >= num_sms * 6) return bn;
+    if (bn32_mode && mt * cdiv(N, 64) * 2 < num_sms) return 32;
     return 64;
   }
 
@@ -779,7 +781,9 @@ struct Engine : EngineBase {
         return;
       }
       if (bn == 0) bn = choose_bn(M, N);
-      if (bn == 64)
+      if (bn == 32)
+        tc_launch<32, 8>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+      else if (bn == 64)
         tc_launch<64, 8>(A, a_cap, lda, M, W, N, K, epi, M_dev);
       else if (bn == 128)
         tc_launch<128, 6>(A, a_cap, lda, M, W, N, K, epi, M_dev);
@@ -1611,7 +1615,10 @@ struct Engine : EngineBase {
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
-    else if (name == "splitk") {
+    else if (name == "bn32") {
+      bn32_mode = value;
+      drop_loop_graphs();
+    } else if (name == "splitk") {
       use_splitk = value != 0;
       drop_loop_graphs();
     }

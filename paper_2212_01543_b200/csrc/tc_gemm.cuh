@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ===== epilogue warps =====
     const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int cbeg = (ew / 4) * (BN / 2), cend = cbeg + BN / 2;  // this warp's column half
+    // this warp's column half (BN = 32: the first four warps take the whole tile)
+    const int cbeg = BN >= 64 ? (ew / 4) * (BN / 2) : 0;
+    const int cend = BN >= 64 ? cbeg + BN / 2 : (ew < 4 ? BN : 0);
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * TC_STG_LD);
     int it = 0;
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);

@@ -93,6 +93,11 @@ bool run(int M, int N, int K) {
 
 int main() {
   bool ok = true;
+  ok &= run<32, 8>(1, 256, 64);
+  ok &= run<32, 8>(800, 384, 128);
+  ok &= run<32, 8>(1000, 512, 512);
+  ok &= run<32, 8>(100, 64, 128);
+  ok &= run<64, 8>(800, 384, 128);
   ok &= run<256, 4>(1, 256, 64);
   ok &= run<128, 6>(1000, 640, 512);
   ok &= run<256, 4>(1, 32000, 512);
