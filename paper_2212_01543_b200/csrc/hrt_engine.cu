@@ -943,21 +943,31 @@ struct Engine : EngineBase {
       // large row counts only (few rows: the warp-per-(row, head) kernel spreads wider); the
       // choice follows the graph's row bucket so graph and eager runs match bit for bit
       const int Rp = path_rows > 0 ? path_rows : R;
-      if (dh == 64 && H <= 16 && (attn_rows_mode == 2 || (attn_rows_mode == 1 && Rp >= 256))) {
+      if (dh == 64 && (H == 1 || H == 2 || H == 4 || H == 8 || H == 16) &&
+          (attn_rows_mode == 2 || (attn_rows_mode == 1 && Rp >= 256))) {
         // one CTA per row, all heads: coalesced whole-row K/V staging
         const size_t smem = attn_rows_smem(d);
-        static bool attr = false;
-        if (!attr) {
-          CUDA_OK(cudaFuncSetAttribute(attn_decode_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)attn_rows_smem(1024)));
-          CUDA_OK(cudaFuncSetAttribute(attn_decode_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)attn_rows_smem(1024)));
-          attr = true;
-        }
         const int threads = std::max(64, H * 32);
-        launch(attn_decode_rows_kernel<SELF>, R, threads, smem, q, qs, kn, vn, ns, kc, vc, d,
-               greedy_hist_identity ? nullptr : hist, greedy_hist_identity ? nullptr : hist2, cap, t, t_dev, row_seq,
-               kv_off, kv_len, R_dev, R, H, att_scale, out, d);
+        auto go = [&](auto kern) {
+          static bool attr = false;
+          if (!attr) {
+            CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_rows_smem(1024)));
+            attr = true;
+          }
+          launch(kern, R, threads, smem, q, qs, kn, vn, ns, kc, vc, d, greedy_hist_identity ? nullptr : hist,
+                 greedy_hist_identity ? nullptr : hist2, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, H, att_scale,
+                 out, d);
+        };
+        if (H == 8)
+          go(attn_decode_rows_kernel<SELF, 8>);
+        else if (H == 16)
+          go(attn_decode_rows_kernel<SELF, 16>);
+        else if (H == 4)
+          go(attn_decode_rows_kernel<SELF, 4>);
+        else if (H == 2)
+          go(attn_decode_rows_kernel<SELF, 2>);
+        else
+          go(attn_decode_rows_kernel<SELF, 1>);
         check_launch();
         return;
       }

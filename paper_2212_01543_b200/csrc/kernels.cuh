@@ -706,7 +706,7 @@ inline size_t attn_rows_smem(int d) {
   return (size_t)2 * AD_KC * (d + AD_PAD) * 2 + (size_t)d * sizeof(float) + AD_KC * sizeof(int);
 }
 
-template <bool SELF>
+template <bool SELF, int HT>  // HT: heads (compile-time index math)
 __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
     const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ knew, const bf16* __restrict__ vnew,
     int new_stride, bf16* __restrict__ kc, bf16* __restrict__ vc, int c_stride, const int* __restrict__ hist_a,
@@ -720,7 +720,9 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
   if (t_dev) t = *t_dev;
   const int r = blockIdx.x;
   if (r >= R) return;
-  const int d = heads * DH, ld = d + AD_PAD, c8n = d / 8;
+  (void)heads;
+  constexpr int d = HT * DH, ld = d + AD_PAD, c8n = d / 8;
+  constexpr int heads_c = HT;
   bf16* Ks = reinterpret_cast<bf16*>(ad_raw);
   bf16* Vs = Ks + AD_KC * ld;
   float* qs = reinterpret_cast<float*>(Vs + AD_KC * ld);
@@ -744,7 +746,7 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
   }
   for (int c = tid; c < d; c += nthr) qs[c] = to_f(q[(size_t)r * q_stride + c]) * scale;
   const int h = warp;
-  const bool active = h < heads;
+  const bool active = h < heads_c;
   float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f;
   for (int j0 = 0; j0 < L; j0 += AD_KC) {
     const int nk = min(AD_KC, L - j0);

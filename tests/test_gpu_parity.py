@@ -436,3 +436,22 @@ def test_decode_attention_row_kernel_matches_head_kernel(hrt, golden):
         assert agree >= len(srcs) - 1, (b_at, agree)
         for a, b in zip(res[2], res[0]):
             assert a.decoder_calls == b.decoder_calls
+
+
+def test_at_translate_protocol_face_matches_reference(hrt, golden):
+    """AT baseline (decoding.py:163-185) driven through the session protocol on
+    the CUDA engine: the reference's own AT runs on the trained fixture."""
+    import os
+
+    from paper_2212_01543_b200 import checkpoint as CK
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    g = golden("tiny_trained")
+    runs = [r for r in g.get("at_runs", [])]
+    if not runs:
+        pytest.skip("fixture has no AT runs")
+    sess = hrt.CudaSession(CK.load_model(os.path.join(here, "tiny_trained.ckpt")), dtype=np.float32, max_beam=4)
+    for r in runs:
+        tr = hrt.at_translate(sess, g["sources"][r["src"]], beam=r["beam"])
+        assert tr.tokens == r["out"]["tokens"]
+        assert abs(tr.score - r["out"]["score"]) <= 1e-3 * max(1.0, abs(r["out"]["score"]))
