@@ -113,10 +113,72 @@ __device__ __forceinline__ uint4 gv_afrag(const bf16* A, int lda, const GvLN& ln
   return u;
 }
 
-template <int NT, int CPW, class Epi, bool LNA = false>
+// Optional LayerNorm tail (residual projections): the last CTA to finish
+// (arrival counter) normalises the M updated rows of x into y, exactly as
+// layernorm_vec_kernel does, so the separate LN launch disappears.
+struct GvTailLN {
+  const float* g;  // nullptr: no tail
+  const float* b;
+  bf16* y;
+  int* counter;  // zero between launches (the last CTA re-arms it)
+};
+
+__device__ __forceinline__ void gv_tail_ln(const float* x, int M, int K, const GvTailLN& t) {
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(t.counter, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = K / 128;
+  for (int r = warp; r < M; r += GV_WARPS) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * K);
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < nv ? __ldcg(xr + lane + 32 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = warp_sum(s) / K;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) {
+        const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+        q += (a * a + bb * bb) + (c * c + e * e);
+      }
+    const float inv = 1.0f / sqrtf(warp_sum(q) / K + 1e-5f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) {
+        const int c4 = (lane + 32 * i) * 4;
+        const float4 gg = *reinterpret_cast<const float4*>(t.g + c4);
+        const float4 bv = *reinterpret_cast<const float4*>(t.b + c4);
+        float4 o;
+        o.x = (v[i].x - mean) * inv * gg.x + bv.x;
+        o.y = (v[i].y - mean) * inv * gg.y + bv.y;
+        o.z = (v[i].z - mean) * inv * gg.z + bv.z;
+        o.w = (v[i].w - mean) * inv * gg.w + bv.w;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(t.y + (size_t)r * K + c4) = u;
+      }
+  }
+  if (threadIdx.x == 0) *t.counter = 0;  // re-arm for the next launch / graph replay
+}
+
+template <int NT, int CPW, class Epi, bool LNA = false, bool TLN = false>
 __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ W, int N, int K, int M,
-                                                                const int* __restrict__ M_dev, Epi epi, GvLN ln) {
+                                                                const int* __restrict__ M_dev, Epi epi, GvLN ln,
+                                                                GvTailLN tln) {
   constexpr int NG = NT < 4 ? NT : 4;  // n-tiles reduced per shared-memory pass
   __shared__ float red[GV_WARPS][NG * 4][32];
   __shared__ float2 lnst[LNA ? 8 * NT : 1];
@@ -201,20 +263,22 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
       }
     }
   }
-  if (!owner) return;
+  if (owner) {
 #pragma unroll
-  for (int o = 0; o < NOWN; ++o) {
-    const int j = o * NG + warp;
-    const int r0 = 8 * j + 2 * t4;
-    if (r0 < M) {
-      if (f0 < N) epi.store2(r0, f0, fin[o][0], pre[o][0]);
-      if (f1 < N) epi.store2(r0, f1, fin[o][2], pre[o][2]);
-    }
-    if (r0 + 1 < M) {
-      if (f0 < N) epi.store2(r0 + 1, f0, fin[o][1], pre[o][1]);
-      if (f1 < N) epi.store2(r0 + 1, f1, fin[o][3], pre[o][3]);
+    for (int o = 0; o < NOWN; ++o) {
+      const int j = o * NG + warp;
+      const int r0 = 8 * j + 2 * t4;
+      if (r0 < M) {
+        if (f0 < N) epi.store2(r0, f0, fin[o][0], pre[o][0]);
+        if (f1 < N) epi.store2(r0, f1, fin[o][2], pre[o][2]);
+      }
+      if (r0 + 1 < M) {
+        if (f0 < N) epi.store2(r0 + 1, f0, fin[o][1], pre[o][1]);
+        if (f1 < N) epi.store2(r0 + 1, f1, fin[o][3], pre[o][3]);
+      }
     }
   }
+  if constexpr (TLN) gv_tail_ln(epi.x, M, N, tln);  // residual epilogue: x rows are N = d wide
 }
 
 // online {max, sum exp} + top-1 (value desc, id asc) over the generable set

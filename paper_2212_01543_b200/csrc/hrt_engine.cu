@@ -311,6 +311,7 @@ struct Engine : EngineBase {
     cudaFree(p_mem);
     cudaFree(sk_ws);
     cudaFree(sk_counters);
+    cudaFree(gv_counter);
     cudaFree(mg_q);
     cudaFree(mg_ctx);
     cudaFree(mg_hid);
@@ -645,6 +646,8 @@ struct Engine : EngineBase {
       CUDA_OK(cudaMalloc(&sk_ws, sk_ws_bytes));
       CUDA_OK(cudaMalloc(&sk_counters, sk_max_tiles * sizeof(int)));
       CUDA_OK(cudaMemset(sk_counters, 0, sk_max_tiles * sizeof(int)));
+      CUDA_OK(cudaMalloc(&gv_counter, 64 * sizeof(int)));
+      CUDA_OK(cudaMemset(gv_counter, 0, 64 * sizeof(int)));
     }
     CUDA_OK(cudaMallocHost(&h_meta, (size_t)meta_cap * sizeof(int)));
     CUDA_OK(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming));
@@ -666,6 +669,7 @@ struct Engine : EngineBase {
   int* sk_counters = nullptr;
   size_t sk_ws_bytes = (size_t)64 << 20;
   int sk_max_tiles = 16384;
+  int* gv_counter = nullptr;  // GEMV LayerNorm-tail arrival counter
   bool use_splitk = false;  // measured slower than unsplit on B200 (fix-up tail); option "splitk"
   int choose_splits(int M, int N, int K, int bn) const {
     if (!use_splitk) return 1;
@@ -726,29 +730,47 @@ struct Engine : EngineBase {
     const int Mp = path_rows > 0 ? path_rows : M;
     return gemv_ok(M, d) && Mp <= 32;
   }
-  template <int NT, int CPW, bool LNA, class Epi>
+  template <int NT, int CPW, bool LNA, bool TLN, class Epi>
   void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
-                     const GvLN& ln) {
-    launch(gemv_small_kernel<NT, CPW, Epi, LNA>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A), lda,
-           reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi, ln);
+                     const GvLN& ln, const GvTailLN& tln) {
+    launch(gemv_small_kernel<NT, CPW, Epi, LNA, TLN>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A),
+           lda, reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi, ln, tln);
   }
-  template <int NT, bool LNA, class Epi>
+  template <int NT, bool LNA, bool TLN, class Epi>
   void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
-                     const GvLN& ln) {
+                     const GvLN& ln, const GvTailLN& tln) {
     const int cpw = std::max(1, K / 32 / GV_WARPS);
-    if (cpw == 1) gemv_launch_t<NT, 1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else if (cpw == 2) gemv_launch_t<NT, 2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else if (cpw == 4) gemv_launch_t<NT, 4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else gemv_launch_t<NT, 8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+    if (cpw == 1) gemv_launch_t<NT, 1, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (cpw == 2) gemv_launch_t<NT, 2, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (cpw == 4) gemv_launch_t<NT, 4, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else gemv_launch_t<NT, 8, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
   }
-  template <bool LNA = false, class Epi>
+  template <bool LNA = false, bool TLN = false, class Epi>
   void gemv_launch(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
-                   const GvLN& ln = GvLN{nullptr, nullptr, nullptr}) {
-    if (M <= 8) gemv_launch_n<1, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else if (M <= 16) gemv_launch_n<2, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else if (M <= 32) gemv_launch_n<4, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else if (M <= 64) gemv_launch_n<8, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
-    else gemv_launch_n<16, LNA>(A, lda, M, W, N, K, epi, M_dev, ln);
+                   const GvLN& ln = GvLN{nullptr, nullptr, nullptr},
+                   const GvTailLN& tln = GvTailLN{nullptr, nullptr, nullptr, nullptr}) {
+    if (M <= 8) gemv_launch_n<1, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (M <= 16) gemv_launch_n<2, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (M <= 32) gemv_launch_n<4, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (M <= 64) gemv_launch_n<8, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else gemv_launch_n<16, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+  }
+  // residual projection followed by a LayerNorm of the updated rows: on the
+  // GEMV path the last CTA normalises (no LN launch), else GEMM + LN kernel
+  bool use_tail_ln = false;  // option "tail_ln" (measured slower than the separate LN launch: off)
+  bool tail_ln_ok(int M, int K) const { return BF16 && use_tail_ln && gemv_ok(M, K) && d % 128 == 0 && d <= 1024; }
+  void gemm_res_ln(const T* A, int a_cap, int lda, int M, const T* W, int K, float* x, const float* bias,
+                   const float* g, const float* b, T* y, const int* M_dev) {
+    if (M <= 0) return;
+    if (tail_ln_ok(M, K)) {
+      Scope sc(this, K_GEMM, (double)sizeof(T) * ((double)d * K + (double)M * K), 2.0 * M * d * K);
+      gemv_launch<false, true>(A, lda, M, W, d, K, EpiResidual{x, d, bias}, M_dev, GvLN{nullptr, nullptr, nullptr},
+                               GvTailLN{g, b, reinterpret_cast<bf16*>(y), gv_counter});
+      check_launch();
+      return;
+    }
+    gemm(K_GEMM, A, a_cap, lda, M, W, d, K, EpiResidual{x, d, bias}, M_dev);
+    layernorm(x, M, g, b, y, nullptr, nullptr, M_dev);
   }
   // LayerNorm feeding a projection: fused into the GEMV prologue on the
   // small-M path (bit-identical operand), else LN kernel + GEMM
@@ -1145,24 +1167,43 @@ struct Engine : EngineBase {
       Tag _tg12(this, "s1.attn_self");
       if (!(s1_skip & 2)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
                         nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd, hist2);
+      // Wo + residual (+ LN2 in the GEMV tail on the small-row path)
+      const bool tail = tail_ln_ok(R, d) && !(s1_skip & 5);
       Tag _tg15(this, "s1.wo");
-      if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
+      if (tail)
+        gemm_res_ln(s1.ctx, R_max, d, R, w.wo, d, s1.x, w.bo, w.ln2g, w.ln2b, s1.y, Rd);
+      else if (!(s1_skip & 4))
+        gemm(K_GEMM, s1.ctx, R_max, d, R, w.wo, d, d, EpiResidual{s1.x, d, w.bo}, Rd);
       Tag _tg19(this, "s1.qc");
-      if (!(s1_skip & 4))
+      if (tail)
+        gemm(K_GEMM, s1.y, R_max, d, R, w.wqc, d, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
+      else if (!(s1_skip & 4))
         gemm_ln(K_GEMM, s1.x, w.ln2g, w.ln2b, s1.y, R_max, R, w.wqc, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
       Tag _tg21(this, "s1.attn_cross");
       if (!(s1_skip & 2)) attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
                          nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
                          2.0 * sizeof(T) * (double)R * max_src * d, nullptr, Rd);
       Tag _tg25(this, "s1.woc");
-      if (!(s1_skip & 4)) gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
+      if (tail)
+        gemm_res_ln(s1.ctx, R_max, d, R, w.woc, d, s1.x, w.boc, w.ln3g, w.ln3b, s1.y, Rd);
+      else if (!(s1_skip & 4))
+        gemm(K_GEMM, s1.ctx, R_max, d, R, w.woc, d, d, EpiResidual{s1.x, d, w.boc}, Rd);
       Tag _tg29(this, "s1.w1");
-      if (!(s1_skip & 4))
+      if (tail)
+        gemm(K_GEMM, s1.y, R_max, d, R, w.w1, ff, d, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
+      else if (!(s1_skip & 4))
         gemm_ln(K_GEMM, s1.x, w.ln3g, w.ln3b, s1.y, R_max, R, w.w1, ff, EpiBiasT<T, true>{s1.hid, ff, w.b1}, Rd);
+      // W2 + residual (+ the next LayerNorm: next layer's LN1 or the final LN)
+      const float* ng = i + 1 < Ld ? dec[i + 1].ln1g : dec_lng;
+      const float* nb = i + 1 < Ld ? dec[i + 1].ln1b : dec_lnb;
+      const bool tail2 = tail && tail_ln_ok(R, ff) && !(i + 1 == Ld && final_ln_fused);
       Tag _tg31(this, "s1.w2");
-      if (!(s1_skip & 4)) gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
+      if (tail2)
+        gemm_res_ln(s1.hid, R_max, ff, R, w.w2, ff, s1.x, w.b2, ng, nb, s1.y, Rd);
+      else if (!(s1_skip & 4))
+        gemm(K_GEMM, s1.hid, R_max, ff, R, w.w2, d, ff, EpiResidual{s1.x, d, w.b2}, Rd);
       Tag _tg34(this, "s1.ln_out");
-      if (s1_skip & 1) {
+      if (s1_skip & 1 || tail2) {
       } else if (i + 1 < Ld)
         layernorm(s1.x, R, dec[i + 1].ln1g, dec[i + 1].ln1b, s1.y, nullptr, nullptr, Rd);
       else if (!final_ln_fused)
@@ -1625,7 +1666,10 @@ struct Engine : EngineBase {
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
       use_graphs = value != 0;
-    else if (name == "bn32") {
+    else if (name == "tail_ln") {
+      use_tail_ln = value != 0;
+      drop_loop_graphs();
+    } else if (name == "bn32") {
       bn32_mode = value;
       drop_loop_graphs();
     } else if (name == "splitk") {
