@@ -418,8 +418,28 @@ def run_engine(args):
         e1.synchronize()
         wall = time.perf_counter() - t0
         ms1 = e0.elapsed_time(e1)
+        # HBM roofline of the batch-1 decode step (north star): per Stage-I step the
+        # decoder + vocabulary weights (w (P_dec + P_voc) bytes) are read once
+        ph = {"encoder": 0.0, "stage1": 0.0, "stage2": 0.0}
+        s1_steps = 0
+        for i in range(n1):
+            eng.translate_arrays(ids1[i], [len(ids1[i])], k=k, b_at=b_at, max_steps=[caps[i]], out=out1)
+            for key, v in eng.phase_times().items():
+                ph[key] += v
+            s1_steps += caps[i]
+        d, ff, V, Ld = sh.d_model, sh.d_ff, sh.vocab_size, sh.dec_layers
+        w_bytes = (2 if spec["dtype"] == "bf16" else 4) * (Ld * (6 * d * d + 2 * d * ff) + V * d)
+        step_us = 1000.0 * ph["stage1"] / max(1, s1_steps)
+        hbm, _, _, _ = peaks()
         batch1 = {"sentences": n1, "ms_per_sentence": ms1 / n1, "target_words_per_s": w1 / (ms1 / 1000.0),
-                  "wall_ms_per_sentence": 1000 * wall / n1, "mode": "e2e host buffers, one sentence per call"}
+                  "wall_ms_per_sentence": 1000 * wall / n1, "mode": "e2e host buffers, one sentence per call",
+                  "phase_ms_per_sentence": {key: v / n1 for key, v in ph.items()},
+                  "stage1_us_per_step": step_us,
+                  "decode_step_roofline": {"bound": "hbm", "bytes_per_step": w_bytes,
+                                           "achieved": w_bytes / (step_us * 1e-6) / 1e9, "peak": hbm, "unit": "GB/s",
+                                           "frac": w_bytes / (step_us * 1e-6) / 1e9 / hbm,
+                                           "note": "algorithmic weight bytes of one batch-1 Stage-I step / its "
+                                                   "device time (decoder layers + tied vocabulary, bf16)"}}
 
     sweep = {}
     if rank == 0 and args.sweep:
