@@ -53,10 +53,14 @@ __global__ void layernorm_vec_kernel(const float* __restrict__ x, const int* __r
   const int orow = out_row ? out_row[row] : row;
   if (orow < 0) return;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
-  float4 v[NV];
+  float4 v[NV], gv[NV], bv[NV];  // gain / bias loads issued with the row (one round trip)
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+  for (int i = 0; i < NV; ++i) {
+    v[i] = xr[lane + 32 * i];
+    gv[i] = __ldg(reinterpret_cast<const float4*>(g) + lane + 32 * i);
+    bv[i] = __ldg(reinterpret_cast<const float4*>(b) + lane + 32 * i);
+  }
 #pragma unroll
   for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   const float mean = warp_sum(s) / d;
@@ -70,13 +74,12 @@ __global__ void layernorm_vec_kernel(const float* __restrict__ x, const int* __r
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c4 = (lane + 32 * i) * 4;
-    const float4 gg = *reinterpret_cast<const float4*>(g + c4);
-    const float4 bv = *reinterpret_cast<const float4*>(b + c4);
+    const float4 gg = gv[i], bb = bv[i];
     float4 o;
-    o.x = (v[i].x - mean) * inv * gg.x + bv.x;
-    o.y = (v[i].y - mean) * inv * gg.y + bv.y;
-    o.z = (v[i].z - mean) * inv * gg.z + bv.z;
-    o.w = (v[i].w - mean) * inv * gg.w + bv.w;
+    o.x = (v[i].x - mean) * inv * gg.x + bb.x;
+    o.y = (v[i].y - mean) * inv * gg.y + bb.y;
+    o.z = (v[i].z - mean) * inv * gg.z + bb.z;
+    o.w = (v[i].w - mean) * inv * gg.w + bb.w;
     store4v<T>(y + (size_t)orow * d + c4, o);
     if (y32) store4v<float>(y32 + (size_t)orow * d + c4, o);
   }
@@ -1267,6 +1270,15 @@ __device__ __forceinline__ void warp_embed_ln_vec(const T* __restrict__ E, const
                                                   T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   float v[NC][8];
+  float4 gq[NC][2], bq[NC][2];  // gain / bias issued with the embedding row (one round trip)
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = (lane + 32 * c) * 8;
+    gq[c][0] = __ldg(reinterpret_cast<const float4*>(g + j));
+    gq[c][1] = __ldg(reinterpret_cast<const float4*>(g + j + 4));
+    bq[c][0] = __ldg(reinterpret_cast<const float4*>(b + j));
+    bq[c][1] = __ldg(reinterpret_cast<const float4*>(b + j + 4));
+  }
   float s = 0.f;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -1295,9 +1307,11 @@ __device__ __forceinline__ void warp_embed_ln_vec(const T* __restrict__ E, const
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int j = (lane + 32 * c) * 8;
+    const float gg[8] = {gq[c][0].x, gq[c][0].y, gq[c][0].z, gq[c][0].w, gq[c][1].x, gq[c][1].y, gq[c][1].z, gq[c][1].w};
+    const float bb[8] = {bq[c][0].x, bq[c][0].y, bq[c][0].z, bq[c][0].w, bq[c][1].x, bq[c][1].y, bq[c][1].z, bq[c][1].w};
     float o[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = (v[c][e] - mean) * inv * g[j + e] + b[j + e];
+    for (int e = 0; e < 8; ++e) o[e] = (v[c][e] - mean) * inv * gg[e] + bb[e];
     *reinterpret_cast<float4*>(x + j) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
     *reinterpret_cast<float4*>(x + j + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
     store4v<T>(y + j, make_float4(o[0], o[1], o[2], o[3]));
