@@ -1162,6 +1162,72 @@ __global__ void rowstats_from_logits_kernel(const float* __restrict__ logits, in
   }
 }
 
+// Top-1 merge (greedy selection / Stage-II argmax): every partial field of a
+// lane's tiles is loaded in one pass (one dependent round trip), then the
+// lane's online {max, sum} and best (value desc, id asc) are warp-reduced.
+// Same results as merge_row<KT>(parts, row, 1): identical max and order of
+// the rescaled sums per lane, identical tie rule.
+__device__ __forceinline__ RowStat merge_row1(const VocabParts& parts, int row) {
+  const int lane = threadIdx.x & 31;
+  const size_t base = (size_t)row * parts.ntiles;
+  constexpr int MAXP = 8;  // tiles per lane held in registers (ntiles <= 256)
+  float pm[MAXP], ps[MAXP], pv[MAXP];
+  int pi[MAXP];
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) {
+    const int t = lane + 32 * i;
+    const bool ok = t < parts.ntiles;
+    const size_t o = base + (ok ? t : 0);
+    pm[i] = ok ? parts.mx[o] : -INFINITY;
+    ps[i] = ok ? parts.sum[o] : 0.f;
+    pv[i] = ok ? parts.val[o] : -INFINITY;
+    pi[i] = ok ? parts.id[o] : 0x7fffffff;
+  }
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) m = fmaxf(m, pm[i]);
+  for (int t = lane + 32 * MAXP; t < parts.ntiles; t += 32) m = fmaxf(m, parts.mx[base + t]);
+  m = warp_max(m);
+  float sm = 0.f, bv = -INFINITY;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) {
+    if (pm[i] != -INFINITY) sm += ps[i] * ex2f((pm[i] - m) * LOG2E);
+    if (pi[i] != 0x7fffffff && better(pv[i], pi[i], bv, bi)) {
+      bv = pv[i];
+      bi = pi[i];
+    }
+  }
+  for (int t = lane + 32 * MAXP; t < parts.ntiles; t += 32) {
+    const float tm = parts.mx[base + t];
+    if (tm != -INFINITY) sm += parts.sum[base + t] * ex2f((tm - m) * LOG2E);
+    const float v = parts.val[base + t];
+    const int id = parts.id[base + t];
+    if (id != 0x7fffffff && better(v, id, bv, bi)) {
+      bv = v;
+      bi = id;
+    }
+  }
+  sm = warp_sum(sm);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  RowStat rs;
+  rs.mx = m;
+  rs.lse = logf(sm);
+  rs.eos = parts.eos[row];
+  rs.kt = 1;
+  rs.val[0] = bv;
+  rs.id[0] = bi;
+  return rs;
+}
+
 // Warp-level merge of a row's tile partials into a RowStat (lane 0 returns it).
 template <int KT>
 __device__ __forceinline__ RowStat merge_row(const VocabParts& parts, int row, int kt) {
@@ -1388,7 +1454,7 @@ __global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, in
   if (st.done[row]) {
     tok = st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
   } else {
-    const RowStat rs = merge_row<KT>(parts, row, 1);
+    const RowStat rs = KT == 1 ? merge_row1(parts, row) : merge_row<KT>(parts, row, 1);
     tok = 0;
     if (lane == 0) {
       const bool last = (t == st.caps[row] - 1);
@@ -1441,7 +1507,7 @@ __global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restr
   if (R_dev) R = *R_dev;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= R) return;
-  const RowStat rs = merge_row<KT>(parts, row, kt);
+  const RowStat rs = (KT == 1 && kt == 1) ? merge_row1(parts, row) : merge_row<KT>(parts, row, kt);
   if ((threadIdx.x & 31) == 0) out[row] = rs;
 }
 
