@@ -994,6 +994,10 @@ struct Engine : EngineBase {
         return;
       }
     }
+    if (greedy_hist_identity) {  // greedy: slot j of row r is row r (no history lookups)
+      hist = nullptr;
+      hist2 = nullptr;
+    }
     const int nwarp = 4;
     lk_max = std::max(lk_max, 1);
     const size_t smem = (size_t)nwarp * lk_max * sizeof(float);

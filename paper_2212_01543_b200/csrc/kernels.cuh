@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   if (R_dev) R = *R_dev;
   if (t_dev) t = *t_dev;
   // beam decoding ping-pongs the history map by step parity (reorder writes the other one)
-  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
+  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;  // nullptr: identity
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * nwarp + warp;
   if (item >= R * heads) return;
@@ -883,18 +883,33 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     L = kv_len[sq];
     kv_row0 = kv_off[sq];
   }
+  // history row of slot j (hist == nullptr: identity, greedy rows never reorder)
+  auto hrow = [&](int j) -> size_t { return hist ? (size_t)hist[(size_t)r * cap + j] : (size_t)r; };
   auto krow = [&](int j) -> const T* {
     if (SELF)
-      return (j == t) ? knew + (size_t)r * new_stride + hoff
-                      : kc + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
+      return (j == t) ? knew + (size_t)r * new_stride + hoff : kc + (hrow(j) * cap + j) * c_stride + hoff;
     return knew + (kv_row0 + j) * (size_t)new_stride + hoff;
   };
   auto vrow = [&](int j) -> const T* {
     if (SELF)
-      return (j == t) ? vnew + (size_t)r * new_stride + hoff
-                      : vc + ((size_t)hist[(size_t)r * cap + j] * cap + j) * c_stride + hoff;
+      return (j == t) ? vnew + (size_t)r * new_stride + hoff : vc + (hrow(j) * cap + j) * c_stride + hoff;
     return vnew + (kv_row0 + j) * (size_t)new_stride + hoff;
   };
+  // PV mapping (see below); the first VPRE keys' V fragments are requested now,
+  // before the scores, so their latency overlaps QK^T and the softmax
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int LPG = DH / VEC >= 1 ? DH / VEC : 1;
+  constexpr int G = 32 / LPG;
+  constexpr int VPRE = 8;
+  const int grp = lane / LPG, li = lane % LPG;
+  uint4 vpre[VPRE];
+  if (DH % VEC == 0 && LPG * VEC == DH) {
+#pragma unroll
+    for (int m = 0; m < VPRE; ++m) {
+      const int j = min(grp + G * m, L - 1);
+      vpre[m] = *reinterpret_cast<const uint4*>(vrow(j) + li * VEC);
+    }
+  }
   float mx = -INFINITY;
   for (int j = lane; j < L; j += 32) {
     const T* kr = krow(j);
@@ -931,15 +946,28 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   const float inv = 1.0f / sum;
   // PV: G groups of LPG lanes; group g takes keys j = g, g+G, ...; a lane owns
   // VEC consecutive head dims and loads them as one 16-byte vector per key.
-  constexpr int VEC = 16 / (int)sizeof(T);
-  constexpr int LPG = DH / VEC >= 1 ? DH / VEC : 1;
-  constexpr int G = 32 / LPG;
-  const int grp = lane / LPG, li = lane % LPG;
   float acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+  int j_start = grp;
+  if (DH % VEC == 0 && LPG * VEC == DH) {
+#pragma unroll
+    for (int m = 0; m < VPRE; ++m) {
+      const int j = grp + G * m;
+      if (j < L) {
+        const float p = sc[j];
+        float vv[VEC];
+        const T* pv = reinterpret_cast<const T*>(&vpre[m]);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) vv[e] = to_f(pv[e]);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = fmaf(p, vv[e], acc[e]);
+      }
+    }
+    j_start = grp + G * VPRE;
+  }
 #pragma unroll 4
-  for (int j = grp; j < L; j += G) {
+  for (int j = j_start; j < L; j += G) {
     const float p = sc[j];
     float vv[VEC];
     loadvec(vrow(j) + li * VEC, vv);
