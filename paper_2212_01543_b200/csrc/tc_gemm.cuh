@@ -244,17 +244,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int c = cbeg; c < cend; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
+          const uint32_t sbase = smem_u32(stg);  // explicit shared-space accesses (not generic ld/st)
 #pragma unroll
           for (int i = 0; i < 8; ++i)  // row `lane`, slot i -> physical slot i ^ (row & 7): conflict-free
-            *reinterpret_cast<float4*>(stg + lane * TC_STG_LD + 4 * (i ^ (lane & 7))) =
-                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             sbase + 4u * (lane * TC_STG_LD + 4 * (i ^ (lane & 7)))),
+                         "f"(v[4 * i]), "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3])
+                         : "memory");
           __syncwarp();
           const int col = n0 + c + (lane & 7) * 4;
           float4 vals[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3);
-            vals[i] = *reinterpret_cast<const float4*>(stg + r * TC_STG_LD + 4 * ((lane & 7) ^ (r & 7)));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(vals[i].x), "=f"(vals[i].y), "=f"(vals[i].z), "=f"(vals[i].w)
+                         : "r"(sbase + 4u * (r * TC_STG_LD + 4 * ((lane & 7) ^ (r & 7))))
+                         : "memory");
           }
           if (S == 1) {
             // rows rbase + (lane >> 3) + 4 i; all global loads of the group are

@@ -11,7 +11,7 @@ caps = W.stage1_caps(srcs, 2)
 ids = np.concatenate([np.asarray(s, np.int32) for s in srcs]); lens = [len(s) for s in srcs]
 for _ in range(2):
     eng.translate_arrays(ids, lens, k=2, max_steps=caps)
-for cls in ("gemm", "vocab", "attn", "other"):
+for cls in ("gemm", "vocab", "attn", "all"):
     eng.timing_enable(cls, True)
     eng.translate_arrays(ids, lens, k=2, max_steps=caps)
     r = eng.timing_read()
