@@ -439,7 +439,7 @@ def run_engine(args):
                                            "achieved": w_bytes / (step_us * 1e-6) / 1e9, "peak": hbm, "unit": "GB/s",
                                            "frac": w_bytes / (step_us * 1e-6) / 1e9 / hbm,
                                            "note": "algorithmic weight bytes of one batch-1 Stage-I step / its "
-                                                   "device time (decoder layers + tied vocabulary, bf16)"}}
+                                                   f"device time (decoder layers + tied vocabulary, {spec['dtype']})"}}
 
     sweep = {}
     if rank == 0 and args.sweep:

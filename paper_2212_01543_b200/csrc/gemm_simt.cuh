@@ -62,3 +62,57 @@ __global__ void __launch_bounds__(SG_THREADS) simt_gemm_kernel(const T* __restri
 }
 
 }  // namespace hrt
+
+namespace hrt {
+
+// fp32 GEMV for the latency-bound shapes (up to GF_MAXM * gridDim.y rows:
+// decode steps, batch-1 encoder / Stage II / vocabulary of the fp32 parity
+// path). One warp per output feature over the full K: lane l reads
+// W[n][k..k+3] for k = 4 l + 128 i as float4 (coalesced 512-byte rows), FFMA
+// against GF_MAXM activation rows (blockIdx.y picks the row block; the weight
+// re-reads of further blocks hit L2), then a fixed-order warp reduction
+// (deterministic). Weights are requested before the PDL grid-dependency wait.
+constexpr int GF_WARPS = 16, GF_MAXM = 8;
+
+template <int KI, class Epi>  // KI: K / 128 (float4 chunks per lane)
+__global__ void __launch_bounds__(GF_WARPS * 32) gemv_f32_kernel(const float* __restrict__ A, int lda,
+                                                                 const float* __restrict__ W, int N, int K, int M,
+                                                                 const int* __restrict__ M_dev, Epi epi) {
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * GF_WARPS + warp;
+  const int nn = n < N ? n : N - 1;
+  float4 w[KI];
+#pragma unroll
+  for (int i = 0; i < KI; ++i) w[i] = __ldg(reinterpret_cast<const float4*>(W + (size_t)nn * K) + lane + 32 * i);
+  pdl_wait();
+  if (M_dev) M = *M_dev;
+  const int r0 = blockIdx.y * GF_MAXM;
+  M -= r0;
+  A += (size_t)r0 * lda;
+  float acc[GF_MAXM];
+#pragma unroll
+  for (int r = 0; r < GF_MAXM; ++r) {
+    acc[r] = 0.f;
+    if (r < M) {
+      const float4* a = reinterpret_cast<const float4*>(A + (size_t)r * lda);
+#pragma unroll
+      for (int i = 0; i < KI; ++i) {
+        const float4 v = a[lane + 32 * i];
+        acc[r] = fmaf(w[i].x, v.x, acc[r]);
+        acc[r] = fmaf(w[i].y, v.y, acc[r]);
+        acc[r] = fmaf(w[i].z, v.z, acc[r]);
+        acc[r] = fmaf(w[i].w, v.w, acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < GF_MAXM; ++r) acc[r] = warp_sum(acc[r]);
+  if (lane == 0 && n < N) {
+#pragma unroll
+    for (int r = 0; r < GF_MAXM; ++r)
+      if (r < M) epi.apply1(r0 + r, n, acc[r]);
+  }
+}
+
+}  // namespace hrt

@@ -721,6 +721,26 @@ struct Engine : EngineBase {
   // captured graph's row bucket instead of the live row count, so eager and
   // graph launches run the same kernels (bit-identical results)
   int path_rows = 0;
+  // fp32 GEMV route (gemv_f32_kernel) for up to gemv_f32_max_m rows; false when the shape does not fit
+  static constexpr int gemv_f32_max_m = 32;
+  template <class Epi>
+  bool gemv_f32(const T* A, int lda, const T* W, int N, int K, int M, int Mp, const int* M_dev, const Epi& epi) {
+    // up to 32 rows always; up to 256 while the 64x64-tile SIMT grid would leave SMs idle
+    const bool small = Mp <= gemv_f32_max_m || (Mp <= 256 && cdiv(Mp, SG_BM) * cdiv(N, SG_BN) < num_sms);
+    if (BF16 || !use_gemv || !small || K % 128 != 0 || K > 16 * 128 || lda % 4 != 0) return false;
+    const float* Af = reinterpret_cast<const float*>(A);
+    const float* Wf = reinterpret_cast<const float*>(W);
+    const dim3 grid(cdiv(N, GF_WARPS), cdiv(Mp, GF_MAXM));
+    switch (K / 128) {
+      case 1: launch(gemv_f32_kernel<1, Epi>, grid, GF_WARPS * 32, 0, Af, lda, Wf, N, K, M, M_dev, epi); break;
+      case 2: launch(gemv_f32_kernel<2, Epi>, grid, GF_WARPS * 32, 0, Af, lda, Wf, N, K, M, M_dev, epi); break;
+      case 4: launch(gemv_f32_kernel<4, Epi>, grid, GF_WARPS * 32, 0, Af, lda, Wf, N, K, M, M_dev, epi); break;
+      case 8: launch(gemv_f32_kernel<8, Epi>, grid, GF_WARPS * 32, 0, Af, lda, Wf, N, K, M, M_dev, epi); break;
+      case 16: launch(gemv_f32_kernel<16, Epi>, grid, GF_WARPS * 32, 0, Af, lda, Wf, N, K, M, M_dev, epi); break;
+      default: return false;
+    }
+    return true;
+  }
   bool gemv_ok(int M, int K) const {
     const int Mp = path_rows > 0 ? path_rows : M;
     return use_gemv && Mp <= gemv_max_m && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
@@ -812,9 +832,12 @@ struct Engine : EngineBase {
       else
         tc_launch<256, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
     } else {
-      dim3 grid(cdiv(N, SG_BN), cdiv(M, SG_BM));
-      launch(simt_gemm_kernel<T, Epi>, grid, SG_THREADS, 0, A, lda, W, K, M, N, K, M_dev, epi,
-                                                                 epi.ld() % 4 == 0);
+      const int Mp = path_rows > 0 ? path_rows : M;
+      if (!gemv_f32(A, lda, W, N, K, M, Mp, M_dev, epi)) {
+        dim3 grid(cdiv(N, SG_BN), cdiv(M, SG_BM));
+        launch(simt_gemm_kernel<T, Epi>, grid, SG_THREADS, 0, A, lda, W, K, M, N, K, M_dev, epi,
+                                                                   epi.ld() % 4 == 0);
+      }
     }
     check_launch();
   }
@@ -1072,9 +1095,11 @@ struct Engine : EngineBase {
           Scope sc(this, K_VOCAB | K_GEMM, 4.0 * ((double)V * d + (double)rn * d + (double)rn * V),
                    2.0 * rn * (double)V * d);
           EpiStoreF32 epi{logits_buf, V};
-          dim3 grid(cdiv(V, SG_BN), cdiv(rn, SG_BM));
-          launch(simt_gemm_kernel<T, EpiStoreF32>, grid, SG_THREADS, 0, y + (size_t)r0 * d, d, E, d, rn, V, d,
-                                                                            nullptr, epi, V % 4 == 0);
+          if (!gemv_f32(y + (size_t)r0 * d, d, E, V, d, rn, rn, nullptr, epi)) {
+            dim3 grid(cdiv(V, SG_BN), cdiv(rn, SG_BM));
+            launch(simt_gemm_kernel<T, EpiStoreF32>, grid, SG_THREADS, 0, y + (size_t)r0 * d, d, E, d, rn, V, d,
+                                                                              nullptr, epi, V % 4 == 0);
+          }
           check_launch();
         }
         VocabParts sub = parts;
