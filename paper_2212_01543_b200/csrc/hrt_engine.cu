@@ -137,6 +137,7 @@ struct EngineBase {
     }
   };
   bool pdl = true;  // programmatic dependent launch on every kernel
+  int launch_cluster = 1;  // cluster size of the next launch (set by tc_launch only)
   template <typename... KArgs, typename... Args>
   void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -144,11 +145,22 @@ struct EngineBase {
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (launch_cluster > 1) {  // thread-block clusters along x (tcgen05 GEMM CTA pairs)
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = launch_cluster;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     cudaError_t er = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
     if (er != cudaSuccess) throw HrtError(HRT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(er));
   }
@@ -682,10 +694,11 @@ struct Engine : EngineBase {
     return S;
   }
 
-  template <int BN, int ST, class Epi>
-  void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+  template <int BN, int ST, class Epi, int CL>
+  void tc_launch_cl(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi,
+                    const int* M_dev) {
     if constexpr (BF16) {
-      auto kern = tc_gemm_kernel<BN, ST, Epi>;
+      auto kern = tc_gemm_kernel<BN, ST, Epi, CL>;
       static bool attr = false;
       const int smem = TcSmem<BN, ST>::TOTAL;
       if (!attr) {
@@ -693,12 +706,27 @@ struct Engine : EngineBase {
         attr = true;
       }
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
-      const CUtensorMap& tb = tmap(W, N, K, K, BN);
-      const int tiles = cdiv(N, BN) * cdiv(M, TC_BM);  // M: count, or upper bound with M_dev
+      const CUtensorMap& tb = tmap(W, N, K, K, BN / CL);
       SplitK sk{1, sk_ws, sk_counters};
-      if constexpr (!Epi::kRowWise) sk.splits = choose_splits(M, N, K, BN);
-      launch(kern, std::min(tiles * sk.splits, num_sms), TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi, sk);
+      if constexpr (!Epi::kRowWise && CL == 1) sk.splits = choose_splits(M, N, K, BN);
+      // M: count, or upper bound with M_dev; CL = 2 works on vertical tile pairs
+      const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL) * sk.splits;
+      const int grid = std::min(units, num_sms / CL) * CL;
+      launch_cluster = CL;
+      launch(kern, grid, TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi, sk);
+      launch_cluster = 1;
     }
+  }
+  // CTA pairs sharing the weight tile (multicast) once there are enough row
+  // tiles to pair up (large-batch encoder / Stage II / vocabulary GEMMs)
+  int cluster_mode = 1;  // option "cluster"
+  int cluster_min_mtiles = 16;
+  template <int BN, int ST, class Epi>
+  void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
+    if (cluster_mode && cdiv(M, TC_BM) >= cluster_min_mtiles && choose_splits(M, N, K, BN) == 1)
+      tc_launch_cl<BN, ST, Epi, 2>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+    else
+      tc_launch_cl<BN, ST, Epi, 1>(A, a_cap, lda, M, W, N, K, epi, M_dev);
   }
 
   // widest N tile that still fills ~0.6 of the SMs (large-M encoder / Stage-II
@@ -1703,6 +1731,13 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "splitk") {
       use_splitk = value != 0;
+      drop_loop_graphs();
+    } else if (name == "cluster") {
+      cluster_mode = value != 0;
+      drop_loop_graphs();
+    } else if (name == "cluster_min_mtiles") {
+      if (value < 2) throw HrtError(HRT_ERR_INVALID, "cluster_min_mtiles >= 2");
+      cluster_min_mtiles = value;
       drop_loop_graphs();
     }
     else if (name == "mega")

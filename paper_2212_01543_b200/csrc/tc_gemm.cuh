@@ -70,7 +70,26 @@ struct EpiRowStore<E, decltype(void(E::kRowStore))> {
   static constexpr bool value = E::kRowStore;
 };
 
-template <int BN, int STAGES, class Epi>
+// B (weight) tile load: whole BN-row box (CL = 1), or this CTA's BN/2-row
+// half multicast to both CTAs of the pair (CL = 2; the tensor map's box is BN/2 rows)
+template <int BN, int CL>
+__device__ __forceinline__ void tc_load_b(uint8_t* dst, const CUtensorMap* tmB, uint64_t* bar, int k0, int n0,
+                                          int crank, uint64_t pol) {
+  if constexpr (CL == 1) {
+    tma_load_2d_hint(dst, tmB, bar, k0, n0, pol);
+  } else {
+    tma_load_2d_mc_hint(dst + crank * (BN / CL) * (TC_BK * 2), tmB, bar, k0, n0 + crank * (BN / CL),
+                        (uint16_t)((1u << CL) - 1), pol);
+  }
+}
+
+// CL = 2: CTA pairs (thread-block clusters of two) take vertically adjacent
+// tiles (m, n) and (m + 1, n); each CTA loads its own A tile and half of the
+// shared B tile, multicast into both CTAs' shared memory, so the L2 -> SM
+// operand traffic per tile drops from (128 + BN) to (128 + BN / 2) rows. A
+// stage is refilled only after both CTAs' MMAs released it (the empty
+// barrier counts one MMA-commit arrival from each CTA). Split-K is CL = 1 only.
+template <int BN, int STAGES, class Epi, int CL = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, const int* __restrict__ M_dev, Epi epi, SplitK sk) {
@@ -83,10 +102,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  static_assert(CL == 1 || CL == 2, "cluster size");
   pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_kb = K / TC_BK;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster index / count
   constexpr uint32_t TMEM_COLS = tmem_cols_for<BN>();
 
   // setup that does not depend on the previous kernel overlaps its tail (PDL)
@@ -95,7 +117,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -105,31 +127,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL > 1)
+    cluster_sync_all();  // the peer's barriers are initialised before any multicast reaches them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles = (N + BN - 1) / BN;
   // work unit = (tile, k-slice); sk.splits > 1 only for element-wise epilogues
-  const int S = sk.splits;
+  const int S = CL > 1 ? 1 : sk.splits;
   // Weights do not depend on the previous kernel: the first unit of a CTA in
   // m-tile 0 (which exists for any M >= 1) gets its first STAGES weight tiles
   // requested before the grid-dependency wait, overlapping the previous
   // kernel's tail (the A tiles follow after the wait into the same stages).
   int pre = 0;
-  if (warp == 0 && lane == 0 && (int)blockIdx.x < n_tiles * S) {
-    const int tile = blockIdx.x / S, ks = blockIdx.x - tile * S;
+  if (warp == 0 && lane == 0 && cid < n_tiles * S) {
+    const int tile = cid / S, ks = cid - tile * S;
     const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
     pre = min(STAGES, kb1 - kb0);
     const uint64_t pol = policy_evict_last();
     for (int s2 = 0; s2 < pre; ++s2) {
       mbar_arrive_expect_tx(&full[s2], L::STAGE_BYTES);
-      tma_load_2d_hint(smem + s2 * L::STAGE_BYTES + L::A_BYTES, &tmB, &full[s2], (kb0 + s2) * TC_BK, tile * BN, pol);
+      tc_load_b<BN, CL>(smem + s2 * L::STAGE_BYTES + L::A_BYTES, &tmB, &full[s2], (kb0 + s2) * TC_BK, tile * BN, crank, pol);
     }
   }
   pdl_wait();
   if (M_dev != nullptr) M = *M_dev;
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
-  const int num_units = m_tiles * n_tiles * S;
+  const int num_units = (m_tiles + CL - 1) / CL * n_tiles * S;  // CL > 1: units are vertical tile pairs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -137,19 +162,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol_w = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = cid; u < num_units; u += ncl) {
         const int tile = u / S, ks = u - tile * S;
-        const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
+        const int m0 = ((tile / n_tiles) * CL + crank) * TC_BM, n0 = (tile % n_tiles) * BN;
         const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
-          if (u == (int)blockIdx.x && kb - kb0 < pre) {  // weight tile already requested before the PDL wait
+          if (u == cid && kb - kb0 < pre) {  // weight tile already requested before the PDL wait
             tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
           } else {
             mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
             tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
-            tma_load_2d_hint(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, pol_w);
+            tc_load_b<BN, CL>(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, crank, pol_w);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -165,7 +190,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      for (int u = cid; u < num_units; u += ncl, ++it) {
         const int ks = u % S;
         const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
         const int acc = it & 1;
@@ -182,7 +207,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < TC_BK / 16; ++k)
             tc_mma_f16(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
                        ((kb - kb0) | k) != 0);
-          tc_commit(&empty[stage]);
+          if constexpr (CL > 1)
+            tc_commit_mc(&empty[stage], (1u << CL) - 1);  // release the stage in both CTAs (B halves are shared)
+          else
+            tc_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -201,11 +229,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * TC_STG_LD);
     int it = 0;
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+    for (int u = cid; u < num_units; u += ncl, ++it) {
       const int tile = u / S, ks = u - tile * S;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int m0 = (tile / n_tiles) * TC_BM, n0 = (tile % n_tiles) * BN;
+      const int m0 = ((tile / n_tiles) * CL + crank) * TC_BM, n0 = (tile % n_tiles) * BN;
       const int rbase = m0 + quarter * 32;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
@@ -320,7 +348,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL > 1)
+    cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);

@@ -70,22 +70,34 @@ struct RowResidual {
   }
 };
 
-template <int BN, int ST, class Epi>
+template <int BN, int ST, class Epi, int CL = 1>
 double timeit(int M, int N, int K, const bf16* A, const bf16* B, const Epi& epi) {
   CUtensorMap ta = make_tmap_bf16_kmajor(A, M, K, K, TC_BM);
-  CUtensorMap tb = make_tmap_bf16_kmajor(B, N, K, K, BN);
-  auto kern = tc_gemm_kernel<BN, ST, Epi>;
+  CUtensorMap tb = make_tmap_bf16_kmajor(B, N, K, K, BN / CL);
+  auto kern = tc_gemm_kernel<BN, ST, Epi, CL>;
   int smem = TcSmem<BN, ST>::TOTAL;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int tiles = ((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
+  int tiles = ((N + BN - 1) / BN) * ((M + TC_BM * CL - 1) / (TC_BM * CL)) * CL;
   dim3 grid(tiles < 148 ? tiles : 148);
-  for (int w = 0; w < 3; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi, SplitK{1, nullptr, nullptr});
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = TC_THREADS;
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&]() { cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr}); };
+  for (int w = 0; w < 3; ++w) go();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
   const int it = 20;
-  for (int w = 0; w < it; ++w) kern<<<grid, TC_THREADS, smem>>>(ta, tb, M, N, K, nullptr, epi, SplitK{1, nullptr, nullptr});
+  for (int w = 0; w < it; ++w) go();
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   if (cudaGetLastError() != cudaSuccess) { printf("launch failed\n"); exit(1); }
@@ -123,16 +135,19 @@ int main() {
       t3 = timeit<256, 4>(M, sh.N, sh.K, A, B, eb);
       t4 = timeit<128, 6>(M, sh.N, sh.K, A, B, eb);
     }
-    double t5;
+    double t5, t6, t7;
     if (sh.N == 512) {
       RowResidual rr{x, 512, bias};
       t5 = timeit<256, 4>(M, sh.N, sh.K, A, B, rr);
+      t6 = timeit<256, 4, EpiResidual, 2>(M, sh.N, sh.K, A, B, er);
     } else {
       RowBias rb{C, sh.N, bias};
       t5 = timeit<256, 4>(M, sh.N, sh.K, A, B, rb);
+      t6 = timeit<256, 4, EpiBiasT<bf16, false>, 2>(M, sh.N, sh.K, A, B, eb);
     }
-    printf("%-4s M=%d N=%d K=%d | null epi: BN256 %.1f us (%.0f TF) BN128 %.1f us (%.0f TF) | real epi: BN256 %.1f us (%.0f TF) BN128 %.1f us (%.0f TF) | row-store BN256 %.1f us (%.0f TF)\n",
-           sh.name, M, sh.N, sh.K, t1, fl / t1 / 1e6, t2, fl / t2 / 1e6, t3, fl / t3 / 1e6, t4, fl / t4 / 1e6, t5, fl / t5 / 1e6);
+    t7 = timeit<256, 4, NullEpi, 2>(M, sh.N, sh.K, A, B, ne);
+    printf("%-4s M=%d N=%d K=%d | null: BN256 %.1f us (%.0f TF) BN128 %.1f (%.0f) CL2 %.1f (%.0f) | real: BN256 %.1f us (%.0f TF) BN128 %.1f (%.0f) CL2 %.1f (%.0f) | row-store BN256 %.1f (%.0f)\n",
+           sh.name, M, sh.N, sh.K, t1, fl / t1 / 1e6, t2, fl / t2 / 1e6, t7, fl / t7 / 1e6, t3, fl / t3 / 1e6, t4, fl / t4 / 1e6, t6, fl / t6 / 1e6, t5, fl / t5 / 1e6);
   }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
