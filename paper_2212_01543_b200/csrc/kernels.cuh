@@ -1983,7 +1983,9 @@ __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* 
   const int i = blockIdx.x;
   if (i >= n) return;
   const int p = perm[i];
-  const int so = src_off[p], len = src_off[p + 1] - so, d0 = dst_off[i];
+  // sources longer than max_len keep their first dst_off[i + 1] - dst_off[i]
+  // tokens (decoding.py:260 truncation); the raw offsets still step over the full source
+  const int so = src_off[p], d0 = dst_off[i], len = min(src_off[p + 1] - so, dst_off[i + 1] - d0);
   for (int j = threadIdx.x; j < len; j += blockDim.x) {
     dst[d0 + j] = src[so + j];
     pos[d0 + j] = j;

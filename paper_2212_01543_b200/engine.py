@@ -200,6 +200,8 @@ class Engine:
         """List of Translation for a list of source id lists (one fused call)."""
         from .decoding import Translation
 
+        if not len(sources):
+            return []  # nothing to decode (the C ABI rejects B < 1)
         t0 = time.perf_counter()
         lens = np.array([len(s) for s in sources], dtype=np.int32)
         ids = np.concatenate([np.asarray(s, dtype=np.int32) for s in sources]) if len(sources) else \

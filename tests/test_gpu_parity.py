@@ -455,3 +455,38 @@ def test_at_translate_protocol_face_matches_reference(hrt, golden):
         tr = hrt.at_translate(sess, g["sources"][r["src"]], beam=r["beam"])
         assert tr.tokens == r["out"]["tokens"]
         assert abs(tr.score - r["out"]["score"]) <= 1e-3 * max(1.0, abs(r["out"]["score"]))
+
+
+def test_edge_sources_match_reference(hrt, golden):
+    """Edge inputs through the fused face vs the fp64 oracle (decoding.py:249-302):
+    an EOS-only source, a source of exactly max_len, one longer than max_len
+    (truncated as decoding.py:260 does), Stage-I caps of 1 (forced EOS at the
+    first step), mixed caps and the uncapped default, every chunk size k, all in
+    one ragged batch; the single-sentence face agrees; an empty batch is []."""
+    g = golden("toy")
+    model = _model(hrt, g)
+    orc = _oracle(g, model)
+    L, V = g["config"]["max_len"], g["config"]["vocab_size"]
+    rng = np.random.default_rng(11)
+
+    def body(n):
+        return [int(x) for x in rng.integers(7, V, n)]
+
+    srcs = [[2], body(L - 1) + [2], body(L + 6) + [2], body(3) + [2], [9, 2]]
+    sess = hrt.CudaSession(model, dtype=np.float32, max_sentences=len(srcs))
+    for k in g["config"]["chunk_sizes"]:
+        for caps in (None, [1] * len(srcs), [1, 3, 2, 5, 4]):
+            out = hrt.hrt_translate_batch(sess, srcs, k, max_steps=caps)
+            assert len(out) == len(srcs)
+            for i, (s, tr) in enumerate(zip(srcs, out)):
+                ref = O.hrt_translate(orc, s, k, max_steps=None if caps is None else caps[i])
+                assert tr.tokens == ref.tokens, (k, caps, i)
+                assert tr.decoder_calls == ref.decoder_calls
+                assert tr.forced == ref.forced
+                for key in ("skip_at_score", "skip_cmlm_score", "score"):
+                    assert abs(getattr(tr, key) - getattr(ref, key)) <= REL * max(1.0, abs(getattr(ref, key))), key
+            one = hrt.hrt_translate(sess, srcs[2], k, max_steps=None if caps is None else caps[2])
+            assert one.tokens == out[2].tokens and one.score == pytest.approx(out[2].score, rel=1e-6)
+    assert hrt.hrt_translate_batch(sess, [], 2) == []
+    with pytest.raises(hrt.DecodingError):
+        hrt.hrt_translate_batch(sess, srcs, 5)
