@@ -490,3 +490,29 @@ def test_edge_sources_match_reference(hrt, golden):
     assert hrt.hrt_translate_batch(sess, [], 2) == []
     with pytest.raises(hrt.DecodingError):
         hrt.hrt_translate_batch(sess, srcs, 5)
+
+
+@pytest.mark.parametrize("b_at,b_nat,B", [(1, 1, 300), (4, 2, 96)])
+def test_large_ragged_batch_matches_reference(hrt, golden, b_at, b_nat, B):
+    """300 sentences in one fp32 fused call: ragged lengths (EOS-only up to past
+    max_len), per-sentence caps from 1 up, so the live-row count crosses every
+    row bucket (512 .. 1) and the kernel regimes chosen per bucket (SIMT GEMM,
+    fp32 GEMV, row and head attention paths); every sentence must equal the fp64
+    oracle's decode of it alone."""
+    g = golden("dh64")
+    model = _model(hrt, g)
+    orc = _oracle(g, model)
+    L, V = g["config"]["max_len"], g["config"]["vocab_size"]
+    rng = np.random.default_rng(23)
+    lens = rng.integers(0, L + 8, B)
+    srcs = [[int(x) for x in rng.integers(7, V, n)] + [2] for n in lens]
+    caps = [int(c) for c in rng.integers(1, 33, B)]
+    sess = hrt.CudaSession(model, dtype=np.float32, max_sentences=B, max_beam=b_at)
+    out = hrt.hrt_translate_batch(sess, srcs, 2, b_at, b_nat, max_steps=caps)
+    bad = []
+    for i, (s, c, tr) in enumerate(zip(srcs, caps, out)):
+        ref = O.hrt_translate(orc, s, 2, b_at, b_nat, max_steps=c)
+        if tr.tokens != ref.tokens or tr.decoder_calls != ref.decoder_calls or \
+                abs(tr.score - ref.score) > REL * max(1.0, abs(ref.score)):
+            bad.append(i)
+    assert not bad, f"{len(bad)} of {B} sentences differ, first {bad[:5]}"
