@@ -516,3 +516,33 @@ def test_large_ragged_batch_matches_reference(hrt, golden, b_at, b_nat, B):
                 abs(tr.score - ref.score) > REL * max(1.0, abs(ref.score)):
             bad.append(i)
     assert not bad, f"{len(bad)} of {B} sentences differ, first {bad[:5]}"
+
+
+def test_bf16_c2_shape_large_batch(hrt):
+    """C2 shape (E12D1, d512, V32000) at 192 sentences, so the tcgen05 paths the
+    benchmark runs are exercised (encoder M ~ 5.6k rows: BN=256 tiles, CTA-pair
+    multicast clusters, all-heads prefill attention; Stage I from 192 rows down
+    through every bucket). The CTA-pair GEMM is bit-identical to the unpaired
+    one; bf16 tokens agree with the (oracle-verified) fp32 engine."""
+    from paper_2212_01543_b200 import workload as W
+
+    spec = W.CONFIGS["c2"]
+    model = hrt.HRTModel.random(spec["shape"], spec["seed"])
+    srcs = W.make_sources(192, 77, spec["lengths"])
+    caps = W.stage1_caps(srcs, 2)
+    eng = hrt.Engine(model, dtype="bfloat16", max_sentences=len(srcs), max_beam=1)
+    a = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("cluster", 0)
+    b = eng.translate_batch(srcs, 2, max_steps=caps)
+    for x, y in zip(a, b):
+        assert x.tokens == y.tokens and x.score == y.score
+    f32 = hrt.Engine(model, dtype="float32", max_sentences=len(srcs), max_beam=1)
+    c = f32.translate_batch(srcs, 2, max_steps=caps)
+    agree = total = 0
+    for x, y in zip(a, c):
+        assert x.decoder_calls == y.decoder_calls
+        total += max(len(x.tokens), len(y.tokens))
+        agree += sum(p == q for p, q in zip(x.tokens, y.tokens))
+    rate = agree / total
+    print(f"C2 bf16 vs fp32 token agreement: {rate:.4f}")
+    assert rate > 0.9
