@@ -355,15 +355,9 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
   float c[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
+  // rolling prefetch: slot i is refilled with chunk cb + GV_MAXC + i as soon as
+  // chunk cb + i is consumed, so GV_MAXC chunks stay in flight per lane
   for (int cb = 0; cb < nch; cb += GV_MAXC) {
-    if (cb > 0) {
-#pragma unroll
-      for (int i = 0; i < GV_MAXC; ++i) {
-        const int ch = min(cb + i, nch - 1);
-        u0[i] = gv_ldw(w0 + 32 * ch, pol);
-        u1[i] = gv_ldw(w1 + 32 * ch, pol);
-      }
-    }
 #pragma unroll
     for (int i = 0; i < GV_MAXC; ++i) {
       if (cb + i < nch) {
@@ -373,6 +367,10 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
           const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (cb + i) + t4 * 8);
           gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
           gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
+        }
+        if (cb + GV_MAXC + i < nch) {
+          u0[i] = gv_ldw(w0 + 32 * (cb + GV_MAXC + i), pol);
+          u1[i] = gv_ldw(w1 + 32 * (cb + GV_MAXC + i), pol);
         }
       }
     }

@@ -137,6 +137,16 @@ struct EngineBase {
     }
   };
   bool pdl = true;  // programmatic dependent launch on every kernel
+  // dynamic shared-memory opt-in per kernel (process-wide: kernels of one
+  // signature share a generic lambda's statics, so the key is the function)
+  template <class K>
+  static void smem_optin(K kern, size_t bytes) {
+    static std::map<const void*, size_t> done;
+    size_t& have = done[reinterpret_cast<const void*>(kern)];
+    if (have >= bytes) return;
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
   int launch_cluster = 1;  // cluster size of the next launch (set by tc_launch only)
   template <typename... KArgs, typename... Args>
   void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
@@ -162,7 +172,14 @@ struct EngineBase {
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t er = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-    if (er != cudaSuccess) throw HrtError(HRT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(er));
+    if (er != cudaSuccess) {
+      const char* fname = nullptr;
+      if (cudaFuncGetName(&fname, reinterpret_cast<const void*>(kern)) != cudaSuccess) fname = "?";
+      throw HrtError(HRT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(er) + " (" + fname + ", grid " +
+                                       std::to_string(grid.x) + "x" + std::to_string(grid.y) + ", block " +
+                                       std::to_string(block.x) + ", smem " + std::to_string(smem) + ", cluster " +
+                                       std::to_string(launch_cluster) + ")");
+    }
   }
   struct Tag {
     EngineBase* e;
@@ -699,12 +716,8 @@ struct Engine : EngineBase {
                     const int* M_dev) {
     if constexpr (BF16) {
       auto kern = tc_gemm_kernel<BN, ST, Epi, CL>;
-      static bool attr = false;
       const int smem = TcSmem<BN, ST>::TOTAL;
-      if (!attr) {
-        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-      }
+      smem_optin(kern, smem);
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN / CL);
       SplitK sk{1, sk_ws, sk_counters};
@@ -960,11 +973,7 @@ struct Engine : EngineBase {
           (attn_heads_mode == 2 || (attn_heads_mode == 1 && n_items >= num_sms))) {
         const size_t smem = attn_heads_smem(d);
         auto go = [&](auto kern) {
-          static bool attr = false;
-          if (!attr) {
-            CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_heads_smem(512)));
-            attr = true;
-          }
+          smem_optin(kern, smem);
           launch(kern, dim3(n_items), 2 * H * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map,
                  kv_off, kv_len, key_ok, causal, att_scale, H);
         };
@@ -1022,11 +1031,7 @@ struct Engine : EngineBase {
         const size_t smem = attn_rows_smem(d);
         const int threads = std::max(64, H * 32);
         auto go = [&](auto kern) {
-          static bool attr = false;
-          if (!attr) {
-            CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_rows_smem(1024)));
-            attr = true;
-          }
+          smem_optin(kern, smem);
           launch(kern, R, threads, smem, q, qs, kn, vn, ns, kc, vc, d, greedy_hist_identity ? nullptr : hist,
                  greedy_hist_identity ? nullptr : hist2, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, H, att_scale,
                  out, d);
@@ -1650,11 +1655,7 @@ struct Engine : EngineBase {
     mp.npf = mega_npf();
     const size_t smem = mega_smem_bytes(d, ff, mp.npf);
     CUDA_OK(cudaMemsetAsync(mg_bar, 0, sizeof(unsigned), stream));
-    static bool attr = false;
-    if (!attr) {
-      CUDA_OK(cudaFuncSetAttribute(decode_mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
-    }
+    smem_optin(decode_mega_kernel, 227 * 1024);
     if (smem > 227 * 1024) throw HrtError(HRT_ERR_INVALID, "megakernel shared memory too large");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms);
