@@ -348,10 +348,7 @@ struct Engine : EngineBase {
     cudaFree(mg_veos);
     cudaFree(mg_bar);
     if (h_meta) cudaFreeHost(h_meta);
-    for (auto& kv : loop_graphs) {
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-    }
+    drop_loop_graphs();
     if (meta_ev) cudaEventDestroy(meta_ev);
   }
 
@@ -372,11 +369,21 @@ struct Engine : EngineBase {
     CUDA_OK(cudaMalloc(&wblob, mats * sizeof(T) + 256));
     CUDA_OK(cudaMalloc(&vblob, vecs * sizeof(float) + 4096));
     stats.weight_bytes = (int64_t)(mats * sizeof(T) + vecs * sizeof(float));
-    T* wp = reinterpret_cast<T*>(wblob);
+    // Stage-I weights (vocabulary E, cross-K/V, decoder layers) are read every
+    // decode step: they go first, contiguous, so one L2 persisting window
+    // covers them; the encoder matrices (used once per batch) follow.
+    hot_bytes = ((size_t)V * d + (size_t)Ld * (8 * d * d + 2 * d * ff)) * sizeof(T);
+    T* wp_hot = reinterpret_cast<T*>(wblob);
+    T* wp = wp_hot + (size_t)V * d + (size_t)Ld * (8 * d * d + 2 * d * ff);
     float* vp = reinterpret_cast<float*>(vblob);
     auto tmat = [&](size_t cnt) {
       T* r = wp;
       wp += cnt;
+      return r;
+    };
+    auto tmat_hot = [&](size_t cnt) {
+      T* r = wp_hot;
+      wp_hot += cnt;
       return r;
     };
     auto tvec = [&](size_t cnt) {
@@ -397,7 +404,7 @@ struct Engine : EngineBase {
     auto put_v = [&](const float* s, int cnt, float* dst) {
       CUDA_OK(cudaMemcpyAsync(dst, s, cnt * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     };
-    E = tmat((size_t)V * d);
+    E = tmat_hot((size_t)V * d);
     convert(src((int64_t)V * d), (size_t)V * d, E);
     enc.resize(Le);
     for (int i = 0; i < Le; ++i) {
@@ -436,16 +443,16 @@ struct Engine : EngineBase {
     put_v(src(d), d, enc_lng);
     put_v(src(d), d, enc_lnb);
     dec.resize(Ld);
-    wxkv = tmat((size_t)Ld * 2 * d * d);
+    wxkv = tmat_hot((size_t)Ld * 2 * d * d);
     bxkv = tvec((size_t)Ld * 2 * d);
     for (int i = 0; i < Ld; ++i) {
       DecW& w = dec[i];
-      w.wqkv = tmat((size_t)3 * d * d);
-      w.wo = tmat((size_t)d * d);
-      w.wqc = tmat((size_t)d * d);
-      w.woc = tmat((size_t)d * d);
-      w.w1 = tmat((size_t)ff * d);
-      w.w2 = tmat((size_t)d * ff);
+      w.wqkv = tmat_hot((size_t)3 * d * d);
+      w.wo = tmat_hot((size_t)d * d);
+      w.wqc = tmat_hot((size_t)d * d);
+      w.woc = tmat_hot((size_t)d * d);
+      w.w1 = tmat_hot((size_t)ff * d);
+      w.w2 = tmat_hot((size_t)d * ff);
       w.bqkv = tvec(3 * d);
       w.bo = tvec(d);
       w.bqc = tvec(d);
@@ -503,7 +510,39 @@ struct Engine : EngineBase {
     CUDA_OK(cudaMemcpyAsync(pe, h_pe.data(), h_pe.size() * sizeof(float), cudaMemcpyHostToDevice, stream));
     CUDA_OK(cudaStreamSynchronize(stream));
     cudaFree(dsrc);
+    if (wp_hot != reinterpret_cast<T*>(wblob) + hot_bytes / sizeof(T))
+      throw HrtError(HRT_ERR_INVALID, "hot weight region layout mismatch");
+    set_l2_persist(l2_persist_mode);
   }
+
+  // L2 persisting window over the Stage-I weights (launches on this stream,
+  // captured graphs included): E and the decoder layers stay L2-resident while
+  // the per-step K/V streams pass through
+  size_t hot_bytes = 0;
+  int l2_persist_mode = 1;  // option "l2_persist"
+  void set_l2_persist(int on) {
+    l2_persist_mode = on;
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    cudaStreamAttrValue av = {};
+    if (on && max_persist > 0 && max_window > 0) {
+      const size_t win = std::min(hot_bytes, (size_t)max_window);
+      const size_t carve = std::min(win, (size_t)max_persist);
+      CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+      av.accessPolicyWindow.base_ptr = wblob;
+      av.accessPolicyWindow.num_bytes = win;
+      av.accessPolicyWindow.hitRatio = std::min(1.0f, (float)carve / (float)win);
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      l2_window_bytes = win;
+    } else {
+      av.accessPolicyWindow.num_bytes = 0;
+      l2_window_bytes = 0;
+    }
+    CUDA_OK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &av));
+  }
+  size_t l2_window_bytes = 0;
 
   static int64_t param_count(const hrt_config& c) {
     int64_t d = c.d_model, f = c.d_ff;
@@ -1673,6 +1712,32 @@ struct Engine : EngineBase {
 
   // Capture (once per row bucket and beam width) the Stage-I step as the body
   // of a conditional WHILE node. Every step-varying value lives in s_ctl.
+  // U consecutive Stage-I steps captured as one plain graph (no conditional
+  // node: every kernel boundary inside keeps its programmatic (PDL) edge)
+  int graph_unroll = 16;  // option "graph_unroll" (0: conditional WHILE loop graph; measured slower)
+  std::map<int, LoopGraph> plain_graphs;
+  LoopGraph& plain_graph(int bucket, int beam, int U, const GreedyState& gs, const BeamState& bs) {
+    LoopGraph& lg = plain_graphs[((bucket * 16 + beam) * 16 + bs.bnat) * 64 + U];
+    if (lg.exec) return lg;
+    const int64_t before = stats.kernel_launches;
+    CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+    try {
+      for (int u = 0; u < U; ++u) {
+        stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
+        launch(stage1_advance_plain_kernel, 1, 1, 0, s_ctl, s_alive);
+        check_launch();
+      }
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(stream, &dummy);
+      throw;
+    }
+    CUDA_OK(cudaStreamEndCapture(stream, &lg.graph));
+    lg.kernels = (int)(stats.kernel_launches - before) / U;
+    stats.kernel_launches = before;
+    CUDA_OK(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+    return lg;
+  }
   LoopGraph& loop_graph(int bucket, int beam, const GreedyState& gs, const BeamState& bs) {
     // captured kernel parameters depend on the bucket, beam and b_nat (finished-store layout)
     LoopGraph& lg = loop_graphs[(bucket * 16 + beam) * 16 + bs.bnat];
@@ -1715,11 +1780,13 @@ struct Engine : EngineBase {
   }
 
   void drop_loop_graphs() {  // options that change kernel choice invalidate the captured loops
-    for (auto& kv : loop_graphs) {
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    for (auto* m : {&loop_graphs, &plain_graphs}) {
+      for (auto& kv : *m) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      }
+      m->clear();
     }
-    loop_graphs.clear();
   }
   void set_option(const std::string& name, int value) override {
     if (name == "graphs")
@@ -1732,6 +1799,12 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "splitk") {
       use_splitk = value != 0;
+      drop_loop_graphs();
+    } else if (name == "graph_unroll") {
+      if (value < 0 || value > 32 || (value & (value - 1))) throw HrtError(HRT_ERR_INVALID, "graph_unroll: 0 or a power of two <= 32");
+      graph_unroll = value;
+    } else if (name == "l2_persist") {
+      set_l2_persist(value != 0);
       drop_loop_graphs();
     } else if (name == "cluster") {
       cluster_mode = value != 0;
@@ -1747,11 +1820,7 @@ struct Engine : EngineBase {
       attn_heads_mode = value;
     else if (name == "attn_rows") {
       attn_rows_mode = value;
-      for (auto& kv : loop_graphs) {
-        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-      }
-      loop_graphs.clear();
+      drop_loop_graphs();
     }
     else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
       if (name == "gemv_max_m") {
@@ -1760,11 +1829,7 @@ struct Engine : EngineBase {
       } else {
         (name == "gemv" ? use_gemv : use_ln_fuse) = value != 0;
       }
-      for (auto& kv : loop_graphs) {  // captured loops bake the GEMM path in
-        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-      }
-      loop_graphs.clear();
+      drop_loop_graphs();
     }
     else if (name == "mega_trace_step")
       mg_trace_step = value;
@@ -1779,11 +1844,7 @@ struct Engine : EngineBase {
     }
     else if (name == "stage1_skip") {
       s1_skip = value;
-      for (auto& kv : loop_graphs) {
-        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-      }
-      loop_graphs.clear();
+      drop_loop_graphs();
     }
     else
       throw HrtError(HRT_ERR_INVALID, "unknown option " + name);
@@ -2072,7 +2133,22 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
       const int hdr[5] = {t0, alive[t0], t0 * k, k, t1};
       CUDA_OK(cudaMemcpyAsync(s_ctl, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream));
     }
-    if (BF16 && use_graphs && timed_class == 0) {
+    if (BF16 && use_graphs && timed_class == 0 && graph_unroll > 0) {
+      // n steps as U-step graphs, U = graph_unroll, graph_unroll / 2, ..., 1
+      // (binary decomposition: at most log2(graph_unroll) + 1 graphs per bucket)
+      int left = t1 - t0;
+      // capture every size of this bucket on first use (no capture inside later timed calls)
+      for (int U = graph_unroll; U >= 1; U >>= 1) plain_graph(bucket, beam, U, gs, bs);
+      for (int U = graph_unroll; U >= 1 && left > 0; U >>= 1) {
+        if (left < U) continue;
+        LoopGraph& lg = plain_graph(bucket, beam, U, gs, bs);
+        while (left >= U) {
+          CUDA_OK(cudaGraphLaunch(lg.exec, stream));
+          stats.kernel_launches += (int64_t)lg.kernels * U;
+          left -= U;
+        }
+      }
+    } else if (BF16 && use_graphs && timed_class == 0) {
       LoopGraph& lg = loop_graph(bucket, beam, gs, bs);
       CUDA_OK(cudaGraphLaunch(lg.exec, stream));
       stats.kernel_launches += (int64_t)lg.kernels * (t1 - t0);

@@ -732,6 +732,8 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
   int* hs = reinterpret_cast<int*>(qs + d);
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
+  uint64_t kv_pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kv_pol));
   int L;
   size_t kv_row0 = 0;
   if (SELF) {
@@ -779,8 +781,13 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
       }
       const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(Ks + j * ld + c));
       const uint32_t sv = static_cast<uint32_t>(__cvta_generic_to_shared(Vs + j * ld + c));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sk), "l"(ksrc) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sv), "l"(vsrc) : "memory");
+      // K/V streams (every row's history / sentence memory, read once per step)
+      // are marked evict-first so they do not push the L2-resident decoder and
+      // vocabulary weights (evict-last) out of L2
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sk), "l"(ksrc), "l"(kv_pol)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sv), "l"(vsrc), "l"(kv_pol)
+                   : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1525,6 +1532,18 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
     ctl->pos = t * ctl->k;
   }
   cudaGraphSetConditional(handle, more ? 1u : 0u);
+}
+
+// Same step advance for the unrolled (plain) loop graphs: the host launches
+// exactly the segment's step count, so no loop condition is set.
+__global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive) {
+  pdl_enter();
+  const int t = ctl->t + 1;
+  if (t < ctl->max_cap && alive[t] > 0) {
+    ctl->t = t;
+    ctl->R = alive[t];
+    ctl->pos = t * ctl->k;
+  }
 }
 
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.

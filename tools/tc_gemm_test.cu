@@ -153,6 +153,10 @@ int main() {
   ok &= run<256, 4>(29300, 512, 2048);
   ok &= run<256, 4, 2>(29300, 512, 2048);
   ok &= run<128, 6, 2>(29300, 512, 2048);
+  ok &= run<256, 4, 1, NullEpi>(1024, 32000, 512);
+  ok &= run<256, 4, 2, NullEpi>(1024, 32000, 512);
+  ok &= run<256, 4, 1, NullEpi>(512, 32000, 512);
+  ok &= run<256, 4, 2, NullEpi>(512, 32000, 512);
   ok &= run<256, 4, 1, NullEpi>(29300, 512, 2048);
   ok &= run<256, 4, 2, NullEpi>(29300, 512, 2048);
   ok &= run<256, 4, 1, NullEpi>(29300, 2048, 512);
