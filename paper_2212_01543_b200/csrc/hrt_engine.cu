@@ -519,7 +519,7 @@ struct Engine : EngineBase {
   // captured graphs included): E and the decoder layers stay L2-resident while
   // the per-step K/V streams pass through
   size_t hot_bytes = 0;
-  int l2_persist_mode = 1;  // option "l2_persist"
+  int l2_persist_mode = 0;  // option "l2_persist" (measured no effect at C2: off, leaves the device L2 limit alone)
   void set_l2_persist(int on) {
     l2_persist_mode = on;
     int max_persist = 0, max_window = 0;
