@@ -775,7 +775,9 @@ struct Engine : EngineBase {
   int cluster_min_mtiles = 16;
   template <int BN, int ST, class Epi>
   void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
-    if (cluster_mode && cdiv(M, TC_BM) >= cluster_min_mtiles && choose_splits(M, N, K, BN) == 1)
+    const int mt = cdiv(M, TC_BM);
+    // wide-N GEMMs (vocabulary) pair up from 4 row tiles: their weight stream dominates L2 -> SM traffic
+    if (cluster_mode && (mt >= cluster_min_mtiles || (mt >= 4 && N >= 8192)) && choose_splits(M, N, K, BN) == 1)
       tc_launch_cl<BN, ST, Epi, 2>(A, a_cap, lda, M, W, N, K, epi, M_dev);
     else
       tc_launch_cl<BN, ST, Epi, 1>(A, a_cap, lda, M, W, N, K, epi, M_dev);

@@ -243,14 +243,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         typename Epi::State st;
         const bool live = row < M;
         if (live) epi.begin(st, row, n0 + cbeg);
+        // software pipeline: chunk c + 32's TMEM load is in flight while chunk c is processed
+        uint32_t ra[32], rb[32];
+        if (cbeg < cend) tmem_ld32_issue(tbase + cbeg, ra);
 #pragma unroll 1
-        for (int c = cbeg; c < cend; c += 32) {
-          float v[32];
-          tmem_ld32(tbase + c, v);
-          const int col0 = n0 + c;
-          int nvalid = N - col0;
-          nvalid = nvalid > 32 ? 32 : nvalid;
-          if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
+        for (int c = cbeg; c < cend; c += 64) {
+          tmem_ld_wait(ra);
+          if (c + 32 < cend) tmem_ld32_issue(tbase + c + 32, rb);
+          {
+            const int col0 = n0 + c;
+            int nvalid = N - col0;
+            nvalid = nvalid > 32 ? 32 : nvalid;
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
+            if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
+          }
+          if (c + 32 < cend) {
+            tmem_ld_wait(rb);
+            if (c + 64 < cend) tmem_ld32_issue(tbase + c + 64, ra);
+            const int col0 = n0 + c + 32;
+            int nvalid = N - col0;
+            nvalid = nvalid > 32 ? 32 : nvalid;
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rb[i]);
+            if (live && nvalid > 0) epi.chunk(st, row, col0, v, nvalid);
+          }
         }
         if (live) epi.end(st, row, n0 + cbeg);
       } else if constexpr (EpiRowStore<Epi>::value) {

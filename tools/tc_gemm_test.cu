@@ -9,6 +9,7 @@
 #include <random>
 #include <type_traits>
 #include "tc_gemm.cuh"
+#include "kernels.cuh"
 #include "tmap.h"
 
 using namespace hrt;
@@ -114,7 +115,67 @@ bool run(int M, int N, int K) {
   return bad == 0;
 }
 
+// timing of the fused vocabulary epilogue (row-wise softmax statistics + top-1)
+template <int CL>
+void time_vocab(int M, int N, int K) {
+  __nv_bfloat16 *dA, *dB;
+  CK(cudaMalloc(&dA, (size_t)M * K * 2));
+  CK(cudaMalloc(&dB, (size_t)N * K * 2));
+  CK(cudaMemset(dA, 0x11, (size_t)M * K * 2));
+  CK(cudaMemset(dB, 0x22, (size_t)N * K * 2));
+  const int bn = 128, nt = (N + bn - 1) / bn;
+  VocabParts parts;
+  CK(cudaMalloc(&parts.mx, (size_t)M * nt * 4));
+  CK(cudaMalloc(&parts.sum, (size_t)M * nt * 4));
+  CK(cudaMalloc(&parts.val, (size_t)M * nt * 4));
+  CK(cudaMalloc(&parts.id, (size_t)M * nt * 4));
+  CK(cudaMalloc(&parts.eos, (size_t)M * 4));
+  parts.ntiles = nt;
+  VocabEpi<1> epi{parts, 0, bn};
+  CUtensorMap ta = make_tmap_bf16_kmajor(dA, M, K, K, TC_BM);
+  CUtensorMap tb = make_tmap_bf16_kmajor(dB, N, K, K, 256 / CL);
+  auto kern = tc_gemm_kernel<256, 4, VocabEpi<1>, CL>;
+  int smem = TcSmem<256, 4>::TOTAL;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int tiles = ((N + 255) / 256) * ((M + TC_BM * CL - 1) / (TC_BM * CL)) * CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles < 148 / CL * CL ? tiles : 148 / CL * CL);
+  cfg.blockDim = TC_THREADS;
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&]() { CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr})); };
+  for (int w = 0; w < 3; ++w) go();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int w = 0; w < 20; ++w) go();
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double us = ms * 1000.0 / 20;
+  printf("vocab CL=%d M=%6d N=%6d K=%5d : %.2f us  %.1f TFLOP/s\n", CL, M, N, K, us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(parts.mx);
+  cudaFree(parts.sum);
+  cudaFree(parts.val);
+  cudaFree(parts.id);
+  cudaFree(parts.eos);
+}
+
 int main() {
+  time_vocab<1>(1024, 32000, 512);
+  time_vocab<2>(1024, 32000, 512);
+  time_vocab<1>(512, 32000, 512);
+  time_vocab<2>(22528, 32000, 512);
   bool ok = true;
   ok &= run<32, 8>(1, 256, 64);
   ok &= run<32, 8>(800, 384, 128);
