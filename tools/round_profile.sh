@@ -9,7 +9,7 @@ timeout 900 python -m pytest tests -m gpu -q > $OUT/${TAG}_pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1
 timeout 600 python bench.py > $OUT/${TAG}_bench.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/${TAG}_bench_ref.log 2>&1
-# launch lists (eager: kernels inside conditional-node graphs cannot be profiled individually)
+# launch lists (eager launches: one ncu record per kernel)
 for B in 1024 1; do
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --profile-from-start off --csv --log-file $OUT/${TAG}_launches_c2_b$B.csv \
