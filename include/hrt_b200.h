@@ -124,8 +124,13 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
                                int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
                                const hrt_translate_out* out, int32_t io_on_device);
 
-/* Engine options: "graphs" (1 = run the Stage-I loop as one captured CUDA
- * graph with a conditional WHILE node, the default; 0 = launch step by step). */
+/* Engine options (all change speed only; results are bit-identical):
+ *   "graphs"        1 (default): Stage-I steps replayed from captured CUDA graphs; 0: launched step by step
+ *   "graph_unroll"  steps per captured graph (power of two <= 32, default 16); 0: one conditional
+ *                   WHILE-node graph per row bucket (the original design, measured slower)
+ *   "cluster"       1 (default): large-M tcgen05 GEMMs as CTA pairs sharing the weight tile
+ *   "gemv", "gemv_max_m", "bn32", "attn_heads", "attn_rows", "splitk", "ln_fuse", "tail_ln",
+ *   "l2_persist", "mega": kernel-path switches documented in DESIGN.md §4 / §7. */
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
 
 /* ---- measurement helpers ------------------------------------------------ */
