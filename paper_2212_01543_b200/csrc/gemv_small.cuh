@@ -55,6 +55,36 @@ __device__ __forceinline__ uint4 gv_ldw(const bf16* p, uint64_t pol) {
   return v;
 }
 
+// Fragment-native weight copy for the GEMV kernels. For output-feature group
+// q (16 rows), 32-wide K chunk ch and half u (rows g / g + 8), the 32 lanes'
+// 16-byte fragments (lane (g, t): row 16 q + g + 8 u, k = 32 ch + 8 t .. + 8)
+// are stored as one contiguous 512-byte run, so every weight load instruction
+// of a warp reads 512 contiguous bytes instead of 8 rows x 64 bytes (the
+// row-major pattern measured 2x slower to stream out of L2). Rows past N are
+// zero. Size: cdiv(N, 16) * 16 * K elements.
+__host__ __device__ constexpr size_t gv_frag_elems(int N, int K) { return (size_t)((N + 15) / 16) * 16 * K; }
+__global__ void gv_frag_layout_kernel(const bf16* __restrict__ W, int N, int K, bf16* __restrict__ out) {
+  const int nch = K / 32;
+  const size_t total = (size_t)((N + 15) / 16) * nch * 2 * 32;  // 16-byte fragments
+  for (size_t f = (size_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (size_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(f & 31);
+    const size_t blk = f >> 5;  // (grp * nch + ch) * 2 + u
+    const int u = (int)(blk & 1);
+    const size_t gc = blk >> 1;
+    const int ch = (int)(gc % nch);
+    const size_t grp = gc / nch;
+    const size_t row = grp * 16 + (lane >> 2) + 8 * u;
+    const int col = 32 * ch + 8 * (lane & 3);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < (size_t)N) v = *reinterpret_cast<const uint4*>(W + row * K + col);
+    *reinterpret_cast<uint4*>(out + f * 8) = v;
+  }
+}
+// base of feature group n0 / 16 in a fragment-native copy; fragment (ch, u) of lane at + ((2 ch + u) * 32 + lane) * 8
+__device__ __forceinline__ const bf16* gv_frag_group(const bf16* Wf, int n0, int K) {
+  return Wf + (size_t)(n0 >> 4) * (K / 32) * 2 * 256;
+}
+
 // Optional LayerNorm prologue (the activation operand is LN(x) of fp32 rows,
 // kernels.py:42-57): the CTA computes every row's statistics exactly as
 // layernorm_vec_kernel does (same lane partition and reduction order, so the
@@ -69,7 +99,7 @@ struct GvLN {
 __device__ __forceinline__ void gv_ln_stats(const GvLN& ln, int M, int K, float2* st) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nv = K / 128;
-  for (int r = warp; r < M; r += GV_WARPS) {
+  for (int r = warp; r < M; r += (int)(blockDim.x >> 5)) {
     const float4* xr = reinterpret_cast<const float4*>(ln.x + (size_t)r * K);
     float4 v[8];
 #pragma unroll
@@ -188,16 +218,17 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   const int nch = K / 32;  // == GV_WARPS * CPW, or fewer chunks than warps with CPW == 1
   const int c0 = warp * CPW, c1 = min(c0 + CPW, nch);
   const int nvalid = N - n0;
-  const bf16* w0 = W + (size_t)(n0 + min(g, nvalid - 1)) * K + t4 * 8;
-  const bf16* w1 = W + (size_t)(n0 + min(g + 8, nvalid - 1)) * K + t4 * 8;
+  (void)nvalid;
+  // W is the fragment-native copy (gv_frag_layout_kernel): rows past N are zero
+  const bf16* wf = gv_frag_group(W, n0, K) + lane * 8;
   // weight fragments: unconditional (clamped) loads keep the arrays in registers
   const uint64_t pol = gv_policy();
   uint4 u0[CPW], u1[CPW];
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     const int ch = min(c0 + i, nch - 1);
-    u0[i] = gv_ldw(w0 + 32 * ch, pol);
-    u1[i] = gv_ldw(w1 + 32 * ch, pol);
+    u0[i] = gv_ldw(wf + (size_t)(2 * ch) * 256, pol);
+    u1[i] = gv_ldw(wf + (size_t)(2 * ch + 1) * 256, pol);
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
@@ -318,16 +349,20 @@ struct GvStat {
   }
 };
 
-constexpr int GV_VTILE = GV_WARPS * 16;  // vocabulary columns per CTA (one partial per row)
+// vocabulary columns per CTA (one partial per row): 8 warps x 16 columns, so
+// the 250 CTAs at V = 32000 spread over every SM (the whole E is streamed from
+// L2 once per step: per-SM L2 bandwidth is the limit)
+constexpr int GV_VWARPS = 8;
+constexpr int GV_VTILE = GV_VWARPS * 16;
 
 // Vocabulary statistics for M <= 8 * NT rows (KT = 1: greedy selection and
 // the Stage-II argmax): parts.ntiles must be cdiv(V, GV_VTILE).
 template <int NT, bool LNA = false>
-__global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
+__global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ E, int V, int K, int M,
                                                                 const int* __restrict__ M_dev, VocabParts parts,
                                                                 int norm_allowed, GvLN ln) {
-  __shared__ float4 ws[GV_WARPS][8 * NT];
+  __shared__ float4 ws[GV_VWARPS][8 * NT];
   __shared__ float2 lnst[LNA ? 8 * NT : 1];
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
@@ -335,16 +370,16 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
   const int nch = K / 32;
   const int nvalid = V - n0;
   const bool has = nvalid > 0;
-  const bf16* w0 = E + (size_t)max(0, min(n0 + g, V - 1)) * K + t4 * 8;
-  const bf16* w1 = E + (size_t)max(0, min(n0 + g + 8, V - 1)) * K + t4 * 8;
+  // E is the fragment-native copy (rows past V zero); CTAs past V read group 0
+  const bf16* wf = gv_frag_group(E, has ? n0 : 0, K) + lane * 8;
   // first batch of weight fragments before the grid-dependency wait
   const uint64_t pol = gv_policy();
   uint4 u0[GV_MAXC], u1[GV_MAXC];
 #pragma unroll
   for (int i = 0; i < GV_MAXC; ++i) {
     const int ch = min(i, nch - 1);
-    u0[i] = gv_ldw(w0 + 32 * ch, pol);
-    u1[i] = gv_ldw(w1 + 32 * ch, pol);
+    u0[i] = gv_ldw(wf + (size_t)(2 * ch) * 256, pol);
+    u1[i] = gv_ldw(wf + (size_t)(2 * ch + 1) * 256, pol);
   }
   pdl_wait();
   if (M_dev) M = *M_dev;
@@ -369,8 +404,8 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
           gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
         }
         if (cb + GV_MAXC + i < nch) {
-          u0[i] = gv_ldw(w0 + 32 * (cb + GV_MAXC + i), pol);
-          u1[i] = gv_ldw(w1 + 32 * (cb + GV_MAXC + i), pol);
+          u0[i] = gv_ldw(wf + (size_t)(2 * (cb + GV_MAXC + i)) * 256, pol);
+          u1[i] = gv_ldw(wf + (size_t)(2 * (cb + GV_MAXC + i) + 1) * 256, pol);
         }
       }
     }
@@ -403,7 +438,7 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_vocab_kernel(const bf16* __re
     GvStat s;
     s.init();
 #pragma unroll 4
-    for (int w = 0; w < GV_WARPS; ++w) {
+    for (int w = 0; w < GV_VWARPS; ++w) {
       const float4 v = ws[w][r];
       s.merge(v.x, v.y, v.z, __float_as_int(v.w));
     }

@@ -333,6 +333,7 @@ struct Engine : EngineBase {
   ~Engine() override {
     cudaSetDevice(device);
     cudaFree(wblob);
+    cudaFree(fblob);
     cudaFree(vblob);
     cudaFree(persist);
     cudaFree(arena);
@@ -513,6 +514,55 @@ struct Engine : EngineBase {
     if (wp_hot != reinterpret_cast<T*>(wblob) + hot_bytes / sizeof(T))
       throw HrtError(HRT_ERR_INVALID, "hot weight region layout mismatch");
     set_l2_persist(l2_persist_mode);
+    if constexpr (BF16) build_frag_weights();
+  }
+
+  // Fragment-native copies of every matrix the GEMV kernels read (gemv_small.cuh:
+  // gv_frag_layout_kernel); the tcgen05 path keeps the K-major originals.
+  char* fblob = nullptr;
+  std::map<const void*, const T*> frag_map;
+  void build_frag_weights() {
+    std::vector<std::tuple<const T*, int, int>> mats;
+    mats.emplace_back(E, V, d);
+    for (const EncW& w : enc) {
+      mats.emplace_back(w.wqkv, 3 * d, d);
+      mats.emplace_back(w.wo, d, d);
+      mats.emplace_back(w.w1, ff, d);
+      mats.emplace_back(w.w2, d, ff);
+    }
+    mats.emplace_back(wxkv, Ld * 2 * d, d);
+    for (const DecW& w : dec) {
+      mats.emplace_back(w.wqkv, 3 * d, d);
+      mats.emplace_back(w.wo, d, d);
+      mats.emplace_back(w.wqc, d, d);
+      mats.emplace_back(w.woc, d, d);
+      mats.emplace_back(w.w1, ff, d);
+      mats.emplace_back(w.w2, d, ff);
+    }
+    size_t total = 0;
+    for (auto& m : mats)
+      if (std::get<2>(m) % 32 == 0) total += gv_frag_elems(std::get<1>(m), std::get<2>(m));
+    if (total == 0) return;
+    CUDA_OK(cudaMalloc(&fblob, total * sizeof(T)));
+    stats.weight_bytes += (int64_t)(total * sizeof(T));
+    T* dst = reinterpret_cast<T*>(fblob);
+    for (auto& m : mats) {
+      const int N = std::get<1>(m), K = std::get<2>(m);
+      if (K % 32) continue;  // the GEMV path requires K % 32 == 0
+      const size_t n16 = gv_frag_elems(N, K) / 8;
+      const int blocks = (int)std::min<size_t>((n16 + 255) / 256, 4096);
+      gv_frag_layout_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const bf16*>(std::get<0>(m)), N, K,
+                                                        reinterpret_cast<bf16*>(dst));
+      check_launch();
+      frag_map[std::get<0>(m)] = dst;
+      dst += gv_frag_elems(N, K);
+    }
+    CUDA_OK(cudaStreamSynchronize(stream));
+  }
+  const T* frag_of(const T* W) const {
+    auto it = frag_map.find(W);
+    if (it == frag_map.end()) throw HrtError(HRT_ERR_INVALID, "GEMV weight without a fragment-native copy");
+    return it->second;
   }
 
   // L2 persisting window over the Stage-I weights (launches on this stream,
@@ -836,7 +886,7 @@ struct Engine : EngineBase {
   void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
                      const GvLN& ln, const GvTailLN& tln) {
     launch(gemv_small_kernel<NT, CPW, Epi, LNA, TLN>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A),
-           lda, reinterpret_cast<const bf16*>(W), N, K, M, M_dev, epi, ln, tln);
+           lda, reinterpret_cast<const bf16*>(frag_of(W)), N, K, M, M_dev, epi, ln, tln);
   }
   template <int NT, bool LNA, bool TLN, class Epi>
   void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
@@ -1122,15 +1172,15 @@ struct Engine : EngineBase {
         parts.ntiles = cdiv(V, GV_VTILE);
         Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
         const bf16* yb = reinterpret_cast<const bf16*>(y);
-        const bf16* Eb = reinterpret_cast<const bf16*>(E);
+        const bf16* Eb = reinterpret_cast<const bf16*>(frag_of(E));
         const GvLN ln{ln_g ? s1.x : nullptr, dec_lng, dec_lnb};
         const int grid = cdiv(V, GV_VTILE);
 #define HRT_GVV(NT)                                                                                          \
   do {                                                                                                       \
     if (ln_g)                                                                                                \
-      launch(gemv_vocab_kernel<NT, true>, grid, GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
+      launch(gemv_vocab_kernel<NT, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
     else                                                                                                     \
-      launch(gemv_vocab_kernel<NT, false>, grid, GV_THREADS, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
+      launch(gemv_vocab_kernel<NT, false>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
   } while (0)
         if (R <= 8)
           HRT_GVV(1);
@@ -1835,7 +1885,10 @@ struct Engine : EngineBase {
     }
     else if (name == "mega_trace_step")
       mg_trace_step = value;
-    else if (name == "mega_skip")
+    else if (name == "s1_skip") {  // debug: skip Stage-I kernel classes (timing attribution only; wrong results)
+      s1_skip = value;
+      drop_loop_graphs();
+    } else if (name == "mega_skip")
       mg_skip = value;
     else if (name == "mega_trace") {
       mg_trace_on = value != 0;
