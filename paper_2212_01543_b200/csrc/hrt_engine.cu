@@ -243,6 +243,9 @@ struct Engine : EngineBase {
   bool use_graphs = true;
   int attn_heads_mode = 1;  // option "attn_heads": all-heads-per-CTA prefill attention (0 off, 1 auto, 2 always)
   int attn_rows_mode = 1;  // option "attn_rows": CTA-per-row decode attention (0 off, 1 >= 256 rows, 2 always)
+  // set in the fused Stage-I loop only: the encoder is complete (a stream copy separates
+  // it from Stage I), so cross-attention K/V may be read before the PDL wait
+  bool cross_prefetch = false;
   bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
@@ -1104,7 +1107,7 @@ struct Engine : EngineBase {
                      const int* kv_off, const int* kv_len, const int* R_dev, int R, int lk_max, T* out) {
     launch(attn_decode_kernel<T, DH, SELF>, blocks, 128, smem, q, qs, kn, vn, ns, kc, vc, d, hist, hist2, cap, t, t_dev,
                                                                   row_seq, kv_off, kv_len, R_dev, R, H, lk_max,
-                                                                  att_scale, out, d);
+                                                                  att_scale, out, d, cross_prefetch ? 1 : 0);
   }
   template <bool SELF>
   void attn_decode(const T* q, int qs, const T* kn, const T* vn, int ns, T* kc, T* vc, const int* hist, int cap, int t,
@@ -2180,11 +2183,17 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     while (b < r) b <<= 1;
     return std::min(b, R_max);
   };
+  struct PrefetchScope {  // cross-attention K/V prefetch is valid inside this loop only
+    bool& f;
+    explicit PrefetchScope(bool& flag) : f(flag) { f = true; }
+    ~PrefetchScope() { f = false; }
+  } pscope(cross_prefetch);
   for (int t0 = 0; t0 < t_mega && alive[t0] > 0;) {
     const int bucket = bucket_of(alive[t0]);
     int t1 = t0;
     while (t1 < t_mega && alive[t1] > 0 && bucket_of(alive[t1]) == bucket) ++t1;
-    if (t0 > 0 || t1 < max_cap) {  // loop control for this segment (the finished count carries over)
+    {  // loop control for this segment (the finished count carries over); the copy also
+       // orders every earlier kernel (encoder) before Stage I (cross_prefetch relies on it)
       const int hdr[5] = {t0, alive[t0], t0 * k, k, t1};
       CUDA_OK(cudaMemcpyAsync(s_ctl, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream));
     }

@@ -5,6 +5,7 @@
 // operands (T) are fp32 or bf16; all reductions accumulate in fp32, and
 // search scores in fp64 as the reference's Python floats do.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace hrt {
@@ -849,9 +850,32 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const int* __restrict__ hist_b, int cap, int t, const int* __restrict__ t_dev, const int* __restrict__ row_seq,
     const int* __restrict__ kv_off,
     const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads, int lk_max, float scale,
-    T* __restrict__ out, int out_stride) {
-  pdl_enter();
+    T* __restrict__ out, int out_stride, int kv_prefetch) {
+  pdl_trigger();
   extern __shared__ float sm[];
+  // Cross attention with kv_prefetch: the sentence memory K/V (and the row ->
+  // sentence metadata) are never written during Stage I, so the first 32 keys'
+  // K fragments are requested before the grid-dependency wait and overlap the
+  // previous kernel (the caller guarantees the encoder finished before Stage I).
+  constexpr bool PRE = !SELF && std::is_same<T, bf16>::value && DH % 8 == 0;
+  uint4 kpre[PRE ? DH / 8 : 1];
+  bool have_pre = false;
+  if constexpr (PRE) {
+    const int item0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int r0 = item0 / heads, h0 = item0 - r0 * heads;
+    if (kv_prefetch && r0 < R) {
+      const int sq = row_seq ? row_seq[r0] : r0;
+      const int L0 = kv_len[sq];
+      const int ln = threadIdx.x & 31;
+      if (ln < L0) {
+        const T* kr = knew + ((size_t)kv_off[sq] + ln) * new_stride + h0 * DH;
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) kpre[c] = *reinterpret_cast<const uint4*>(kr + 8 * c);
+      }
+      have_pre = true;
+    }
+  }
+  pdl_wait();
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;
   if (R_dev) R = *R_dev;
   if (t_dev) t = *t_dev;
@@ -925,7 +949,21 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
 #pragma unroll
       for (int c = 0; c < DH; c += 8) {
         float kk[8];
-        load8(kr + c, kk);
+        if constexpr (PRE) {
+          if (have_pre && j == lane) {  // prefetched fragment (same conversion as load8)
+            const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&kpre[c / 8]);
+#pragma unroll
+            for (int i2 = 0; i2 < 4; ++i2) {
+              const float2 f = __bfloat1622float2(hp[i2]);
+              kk[2 * i2] = f.x;
+              kk[2 * i2 + 1] = f.y;
+            }
+          } else {
+            load8(kr + c, kk);
+          }
+        } else {
+          load8(kr + c, kk);
+        }
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
           a0 = fmaf(qr[c + e], kk[e], a0);
