@@ -1128,7 +1128,7 @@ struct Engine : EngineBase {
           smem_optin(kern, smem);
           launch(kern, R, threads, smem, q, qs, kn, vn, ns, kc, vc, d, greedy_hist_identity ? nullptr : hist,
                  greedy_hist_identity ? nullptr : hist2, cap, t, t_dev, row_seq, kv_off, kv_len, R_dev, R, H, att_scale,
-                 out, d);
+                 out, d, cross_prefetch ? 1 : 0);
         };
         if (H == 8)
           go(attn_decode_rows_kernel<SELF, 8>);

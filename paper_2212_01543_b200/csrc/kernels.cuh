@@ -716,15 +716,10 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
     int new_stride, bf16* __restrict__ kc, bf16* __restrict__ vc, int c_stride, const int* __restrict__ hist_a,
     const int* __restrict__ hist_b, int cap, int t, const int* __restrict__ t_dev, const int* __restrict__ row_seq,
     const int* __restrict__ kv_off, const int* __restrict__ kv_len, const int* __restrict__ R_dev, int R, int heads,
-    float scale, bf16* __restrict__ out, int out_stride) {
-  pdl_enter();
+    float scale, bf16* __restrict__ out, int out_stride, int kv_prefetch) {
+  pdl_trigger();
   constexpr int DH = 64;
   extern __shared__ __align__(16) unsigned char ad_raw[];
-  if (R_dev) R = *R_dev;
-  if (t_dev) t = *t_dev;
-  const int r = blockIdx.x;
-  if (r >= R) return;
-  (void)heads;
   constexpr int d = HT * DH, ld = d + AD_PAD, c8n = d / 8;
   constexpr int heads_c = HT;
   bf16* Ks = reinterpret_cast<bf16*>(ad_raw);
@@ -732,9 +727,41 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
   float* qs = reinterpret_cast<float*>(Vs + AD_KC * ld);
   int* hs = reinterpret_cast<int*>(qs + d);
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
-  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
   uint64_t kv_pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kv_pol));
+  const int r = blockIdx.x;
+  // cross attention with kv_prefetch: the sentence memory (immutable during
+  // Stage I) streams its first key chunk into shared memory before the
+  // grid-dependency wait, overlapping the previous kernel
+  bool pre = false;
+  if (!SELF && kv_prefetch && r < R) {
+    const int sq = row_seq ? row_seq[r] : r;
+    const int nk0 = min(AD_KC, kv_len[sq]);
+    const size_t row0 = kv_off[sq];
+    for (int idx = tid; idx < nk0 * c8n; idx += nthr) {
+      const int j = idx / c8n, c = (idx - j * c8n) * 8;
+      const size_t pr = (row0 + j) * (size_t)new_stride + c;
+      const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(Ks + j * ld + c));
+      const uint32_t sv = static_cast<uint32_t>(__cvta_generic_to_shared(Vs + j * ld + c));
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sk), "l"(knew + pr),
+                   "l"(kv_pol)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sv), "l"(vnew + pr),
+                   "l"(kv_pol)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    pre = true;
+  }
+  pdl_wait();
+  if (R_dev) R = *R_dev;
+  if (t_dev) t = *t_dev;
+  if (r >= R) {
+    asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may outlive the CTA
+    return;
+  }
+  (void)heads;
+  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;
   int L;
   size_t kv_row0 = 0;
   if (SELF) {
@@ -761,7 +788,7 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
       for (int j = tid; j < nk; j += nthr) hs[j] = hist[(size_t)r * cap + j0 + j];
       __syncthreads();
     }
-    for (int idx = tid; idx < nk * c8n; idx += nthr) {
+    for (int idx = tid; idx < ((pre && j0 == 0) ? 0 : nk * c8n); idx += nthr) {  // chunk 0 prefetched
       const int j = idx / c8n, c = (idx - j * c8n) * 8;
       const bf16* ksrc;
       const bf16* vsrc;
