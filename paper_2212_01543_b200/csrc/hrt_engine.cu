@@ -246,6 +246,7 @@ struct Engine : EngineBase {
   // set in the fused Stage-I loop only: the encoder is complete (a stream copy separates
   // it from Stage I), so cross-attention K/V may be read before the PDL wait
   bool cross_prefetch = false;
+  int debug_spin_us = 0;  // option "debug_spin" (host-bound vs device-bound attribution)
   bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
@@ -1855,6 +1856,8 @@ struct Engine : EngineBase {
     } else if (name == "splitk") {
       use_splitk = value != 0;
       drop_loop_graphs();
+    } else if (name == "debug_spin") {
+      debug_spin_us = value;
     } else if (name == "graph_unroll") {
       if (value < 0 || value > 32 || (value & (value - 1))) throw HrtError(HRT_ERR_INVALID, "graph_unroll: 0 or a power of two <= 32");
       graph_unroll = value;
@@ -2138,6 +2141,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     launch(gather_sentences_kernel, B, 128, 0, src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B);
     check_launch();
   }
+  if (debug_spin_us > 0) debug_spin_kernel<<<1, 32, 0, stream>>>((long long)debug_spin_us * 1000);
   // ---- phase 1: encoder ----
   phase_mark(0);
   run_encoder(Mtok, B, max_src, d_off, d_len, d_enc_items, (int)enc_items.size() / 2);

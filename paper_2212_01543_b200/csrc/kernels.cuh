@@ -2077,6 +2077,15 @@ __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* 
 }
 
 // Stage-I row initialisation: feed = bos, history slot map = identity.
+// Debug (option "debug_spin"): occupy the stream for `ns` nanoseconds so the
+// host runs ahead; phase times measured behind it are pure device time.
+__global__ void debug_spin_kernel(long long ns) {
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  long long t1 = t0;
+  while (t1 - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+}
+
 __global__ void stage1_init_kernel(int R, int cap, int bos, int* feed, int* done, int* nsteps, int* forced,
                                    double* score, int* hist) {
   pdl_enter();
