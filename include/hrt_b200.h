@@ -124,7 +124,8 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
                                int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
                                const hrt_translate_out* out, int32_t io_on_device);
 
-/* Engine options (all change speed only; results are bit-identical):
+/* Engine options (speed only; "graphs", "graph_unroll", "cluster" are bit-identical, the kernel-path
+ * switches change the bf16 summation order):
  *   "graphs"        1 (default): Stage-I steps replayed from captured CUDA graphs; 0: launched step by step
  *   "graph_unroll"  steps per captured graph (power of two <= 32, default 16); 0: one conditional
  *                   WHILE-node graph per row bucket (the original design, measured slower)
