@@ -266,6 +266,8 @@ struct Engine : EngineBase {
   double* o_scores;
   unsigned char* o_forced;
   int* h_meta = nullptr;  // pinned staging for per-call metadata (one H2D copy)
+  char* h_out = nullptr;  // pinned staging for the packed per-call outputs (one D2H copy)
+  size_t h_out_bytes = 0;
   int meta_cap;
   size_t meta_hdr = 0;     // ints reserved at the start for the fixed header
   cudaEvent_t meta_ev = nullptr;
@@ -353,6 +355,7 @@ struct Engine : EngineBase {
     cudaFree(mg_veos);
     cudaFree(mg_bar);
     if (h_meta) cudaFreeHost(h_meta);
+    if (h_out) cudaFreeHost(h_out);
     drop_loop_graphs();
     if (meta_ev) cudaEventDestroy(meta_ev);
   }
@@ -772,6 +775,8 @@ struct Engine : EngineBase {
       CUDA_OK(cudaMemset(gv_counter, 0, 64 * sizeof(int)));
     }
     CUDA_OK(cudaMallocHost(&h_meta, (size_t)meta_cap * sizeof(int)));
+    h_out_bytes = (size_t)Bmax * Lmax * sizeof(int) + 2 * (size_t)Bmax * sizeof(int) + 8 + (size_t)Bmax * 3 * sizeof(double) + Bmax;
+    CUDA_OK(cudaMallocHost(&h_out, h_out_bytes));
     CUDA_OK(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming));
     CUDA_OK(cudaEventRecord(meta_ev, stream));
   }
@@ -2264,6 +2269,20 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   so.scores = host_io ? o_scores : out->scores;
   so.calls = host_io ? o_calls : out->calls;
   so.forced = host_io ? o_forced : out->forced;
+  // synchronous host I/O: the five outputs of this call are packed back to back
+  // (sized by B, inside the o_* region) so one D2H copy returns them all
+  const size_t pk_len = (size_t)B * Lmax * sizeof(int), pk_calls = pk_len + B * sizeof(int),
+               pk_scores = align_up(pk_calls + B * sizeof(int), 8), pk_forced = pk_scores + (size_t)B * 3 * sizeof(double),
+               pk_total = pk_forced + B;
+  const bool packed = host_io && on_device == 0 && h_out != nullptr && pk_total <= h_out_bytes;
+  if (packed) {
+    char* pb = reinterpret_cast<char*>(o_tokens);
+    so.tokens = reinterpret_cast<int*>(pb);
+    so.lens = reinterpret_cast<int*>(pb + pk_len);
+    so.calls = reinterpret_cast<int*>(pb + pk_calls);
+    so.scores = reinterpret_cast<double*>(pb + pk_scores);
+    so.forced = reinterpret_cast<unsigned char*>(pb + pk_forced);
+  }
   so.out_index = d_perm;
   {
     Scope sc(this, K_OTHER, 0, 0);
@@ -2273,7 +2292,16 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   phase_mark(3);
   phase_valid = true;
-  if (host_io) {
+  if (packed) {
+    CUDA_OK(cudaMemcpyAsync(h_out, o_tokens, pk_total, cudaMemcpyDeviceToHost, stream));
+    CUDA_OK(cudaStreamSynchronize(stream));
+    std::memcpy(out->tokens, h_out, pk_len);
+    std::memcpy(out->lens, h_out + pk_len, B * sizeof(int));
+    std::memcpy(out->calls, h_out + pk_calls, B * sizeof(int));
+    std::memcpy(out->scores, h_out + pk_scores, (size_t)B * 3 * sizeof(double));
+    std::memcpy(out->forced, h_out + pk_forced, B);
+    for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+  } else if (host_io) {
     CUDA_OK(cudaMemcpyAsync(out->tokens, o_tokens, (size_t)B * Lmax * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->lens, o_lens, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->scores, o_scores, B * 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
