@@ -691,7 +691,8 @@ struct Engine : EngineBase {
 
   void alloc_buffers() {
     // persistent region
-    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256 + 8 + 2 * (cap_max + 8) + 2 * (Bmax + 16);
+    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256 + 8 + 2 * (cap_max + 8) + 2 * (Bmax + 16) +
+               Me_max + Bmax + 8;  // + the call's source ids
     auto persist_plan = [&](char* base) {
       Plan p;
       d_ids_raw = p.take<int>(base, Me_max + Bmax);
@@ -2124,6 +2125,14 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   const std::vector<int> enc_items = prefill_items(len), s2_items = prefill_items(slot);
   int* d_enc_items = meta_put(cur, enc_items);
   int* d_s2_items = meta_put(cur, s2_items);
+  // host source ids ride in the same pinned metadata copy (one H2D transfer per call)
+  const bool host_io = on_device != 1;
+  int* d_ids_meta = nullptr;
+  if (host_io && cur + raw_off[B] <= (size_t)meta_cap) {
+    std::memcpy(h_meta + cur, ids, (size_t)raw_off[B] * sizeof(int));
+    d_ids_meta = d_meta + cur;
+    cur = (cur + raw_off[B] + 7) & ~size_t(7);
+  }
   {  // fixed header: loop control + alive[] + source offsets/lengths
     StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, B, 0, 0};
     std::memcpy(h_meta, &c, sizeof(StepCtl));
@@ -2136,8 +2145,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   meta_flush(cur);
   const int* src_ids = ids;
-  const bool host_io = on_device != 1;
-  if (host_io) {
+  if (d_ids_meta) {
+    src_ids = d_ids_meta;
+  } else if (host_io) {
     CUDA_OK(cudaMemcpyAsync(d_ids_raw, ids, raw_off[B] * sizeof(int), cudaMemcpyHostToDevice, stream));
     src_ids = d_ids_raw;
   }
