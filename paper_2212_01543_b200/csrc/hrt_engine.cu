@@ -246,7 +246,8 @@ struct Engine : EngineBase {
   // set in the fused Stage-I loop only: the encoder is complete (a stream copy separates
   // it from Stage I), so cross-attention K/V may be read before the PDL wait
   bool cross_prefetch = false;
-  int debug_spin_us = 0;  // option "debug_spin" (host-bound vs device-bound attribution)
+  int debug_spin_us = 0;
+  int enc_skip = 0;  // option "enc_skip" (debug attribution of the encoder kernels)  // option "debug_spin" (host-bound vs device-bound attribution)
   bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
   bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
   bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
@@ -1290,19 +1291,22 @@ struct Engine : EngineBase {
       embed_ln(d_ids, d_pos, 0, M, enc[0].ln1g, enc[0].ln1b, eb.x, eb.y);
     else
       embed_ln(d_ids, d_pos, 0, M, enc_lng, enc_lnb, eb.x, eb.y);
+    const int sk = enc_skip;  // debug attribution: 1 LN, 2 attention, 4 projections (wrong results)
     for (int i = 0; i < Le; ++i) {
       const EncW& w = enc[i];
-      gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
-      attn_prefill(items, n_items, eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, off, len, len,
-                   nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
-      gemm(K_GEMM, eb.ctx, Me_max, d, M, w.wo, d, d, EpiResidual{eb.x, d, w.bo});
-      layernorm(eb.x, M, w.ln2g, w.ln2b, eb.y);
-      gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
-      gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
-      if (i + 1 < Le)
-        layernorm(eb.x, M, enc[i + 1].ln1g, enc[i + 1].ln1b, eb.y);
-      else
+      if (!(sk & 4)) gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
+      if (!(sk & 2))
+        attn_prefill(items, n_items, eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, off, len, len,
+                     nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
+      if (!(sk & 4)) gemm(K_GEMM, eb.ctx, Me_max, d, M, w.wo, d, d, EpiResidual{eb.x, d, w.bo});
+      if (!(sk & 1)) layernorm(eb.x, M, w.ln2g, w.ln2b, eb.y);
+      if (!(sk & 4)) gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
+      if (!(sk & 4)) gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
+      if (i + 1 < Le) {
+        if (!(sk & 1)) layernorm(eb.x, M, enc[i + 1].ln1g, enc[i + 1].ln1b, eb.y);
+      } else {
         layernorm(eb.x, M, enc_lng, enc_lnb, eb.y, nullptr, p_mem_target);
+      }
     }
     gemm(K_GEMM, eb.y, Me_max, d, M, wxkv, Ld * 2 * d, d, EpiBiasT<T, false>{xkv, Ld * 2 * d, bxkv});
   }
@@ -1862,6 +1866,8 @@ struct Engine : EngineBase {
     } else if (name == "splitk") {
       use_splitk = value != 0;
       drop_loop_graphs();
+    } else if (name == "enc_skip") {
+      enc_skip = value;
     } else if (name == "debug_spin") {
       debug_spin_us = value;
     } else if (name == "graph_unroll") {
