@@ -374,6 +374,7 @@ def run_engine(args):
     eng.timing_enable("gemm", True)
     run_device(one, 1)
     g = eng.timing_read()
+    g_sites = eng.timing_report()  # per call site: (ms, launches, FLOPs)
     eng.timing_enable("gemm", False)
     eng.timing_enable("vocab", True)
     run_device(one, 1)
@@ -474,6 +475,14 @@ def run_engine(args):
             "gemm_ms_per_step": g["ms"], "gemm_launches_per_step": g["launches"],
             "gemm_share_of_step": g["ms"] / ms_all if ms_all else None,
             "vocab_ms_per_step": vv["ms"], "vocab_tflops": vv["flops"] / (vv["ms"] / 1e3) / 1e12 if vv["ms"] else None,
+            # the same GEMM class split by phase: large-M encoder / Stage-II GEMMs vs the
+            # latency-bound per-step Stage-I projections (SURVEY 8(d) per-phase bounds)
+            "gemm_by_phase": {
+                ph: {"ms": sum(v[0] for k2, v in g_sites.items() if k2.split(".")[0] == ph),
+                     "tflops": (sum(v[2] for k2, v in g_sites.items() if k2.split(".")[0] == ph) /
+                                (sum(v[0] for k2, v in g_sites.items() if k2.split(".")[0] == ph) / 1e3) / 1e12)
+                     if sum(v[0] for k2, v in g_sites.items() if k2.split(".")[0] == ph) else None}
+                for ph in ("encoder", "s1", "stage2")},
             "all_kernels_ms_per_step": allk["ms"], "instrumented_step_ms": ms_all}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,

@@ -86,6 +86,7 @@ struct EngineBase {
   int timed_class = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   std::vector<const char*> ev_tag;
+  std::vector<double> ev_flops;  // algorithmic FLOPs of each timed launch
   size_t ev_used = 0;
   const char* cur_tag = "untagged";  // call-site tag for the next launches
   double t_bytes = 0, t_flops = 0;
@@ -123,7 +124,9 @@ struct EngineBase {
           e->ev_pool.emplace_back(a, b);
         }
         if (e->ev_tag.size() < e->ev_pool.size()) e->ev_tag.resize(e->ev_pool.size());
+        if (e->ev_flops.size() < e->ev_pool.size()) e->ev_flops.resize(e->ev_pool.size());
         e->ev_tag[e->ev_used] = e->cur_tag;
+        e->ev_flops[e->ev_used] = flops;
         ev = &e->ev_pool[e->ev_used++];
         cudaEventRecord(ev->first, e->stream);
         e->t_bytes += bytes;
@@ -2473,18 +2476,24 @@ hrt_status hrt_timing_report(hrt_engine* eng, char* buf, int64_t cap) {
   return guarded(eng, [&] {
     EngineBase* e = eng->impl.get();
     CUDA_OK(cudaStreamSynchronize(e->stream));
-    std::map<std::string, std::pair<double, int>> agg;
+    struct Agg {
+      double ms = 0, flops = 0;
+      int n = 0;
+    };
+    std::map<std::string, Agg> agg;
     for (size_t i = 0; i < e->ev_used; ++i) {
       float m = 0;
       CUDA_OK(cudaEventElapsedTime(&m, e->ev_pool[i].first, e->ev_pool[i].second));
-      auto& a = agg[e->ev_tag[i] ? e->ev_tag[i] : "untagged"];
-      a.first += m;
-      a.second += 1;
+      Agg& a = agg[e->ev_tag[i] ? e->ev_tag[i] : "untagged"];
+      a.ms += m;
+      a.n += 1;
+      a.flops += e->ev_flops[i];
     }
     std::string s = "{";
     for (auto& kv : agg) {
       if (s.size() > 1) s += ", ";
-      s += "\"" + kv.first + "\": [" + std::to_string(kv.second.first) + ", " + std::to_string(kv.second.second) + "]";
+      s += "\"" + kv.first + "\": [" + std::to_string(kv.second.ms) + ", " + std::to_string(kv.second.n) + ", " +
+           std::to_string(kv.second.flops) + "]";
     }
     s += "}";
     if ((int64_t)s.size() + 1 > cap) throw HrtError(HRT_ERR_INVALID, "report buffer too small");

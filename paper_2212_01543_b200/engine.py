@@ -139,7 +139,7 @@ class Engine:
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 
     def timing_report(self):
-        """{call-site tag: (device ms, launches)} of the timed launches since timing_enable."""
+        """{call-site tag: (device ms, launches, algorithmic FLOPs)} of the timed launches since timing_enable."""
         import json
 
         buf = C.create_string_buffer(1 << 16)

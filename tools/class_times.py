@@ -18,5 +18,5 @@ for cls in ("gemm", "vocab", "attn", "all"):
     rep = eng.timing_report()
     eng.timing_enable(cls, False)
     print(f"{cls:6s} {r['ms']:8.3f} ms {r['launches']:6d} launches  flops {r['flops']/1e9:9.1f} G  -> {r['flops']/(r['ms']*1e-3)/1e12 if r['ms'] else 0:7.1f} TFLOP/s")
-    for k, (ms, n) in sorted(rep.items(), key=lambda x: -x[1][0])[:8]:
+    for k, (ms, n, _f) in sorted(rep.items(), key=lambda x: -x[1][0])[:8]:
         print(f"     {k:18s} {ms:8.3f} ms {n:6d}")

@@ -33,7 +33,7 @@ def main():
     tot = sum(v[0] for v in rep.values())
     steps = max(caps)
     print(f"batch {a.batch}: {tot:.3f} ms in timed launches, Stage-I steps {steps}")
-    for k, (ms, n) in sorted(rep.items(), key=lambda x: -x[1][0]):
+    for k, (ms, n, _f) in sorted(rep.items(), key=lambda x: -x[1][0]):
         print(f"  {k:18s} {ms:8.3f} ms {n:6d} launches {1000*ms/n:8.2f} us/launch")
     eng.translate_arrays(ids, lens, k=spec["k"], b_at=spec["beam"], max_steps=caps)
     print("graph-mode phases (ms):", eng.phase_times())
