@@ -178,3 +178,24 @@ def test_cli_parser():
     assert a.b_at == 4 and a.k == 2 and a.input == "-"
     a = cli.build_parser().parse_args(["bench", "--checkpoint", "m", "--vocab", "v", "--corpus", "c"])
     assert a.runs == 5
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the reference CPU path, runnable without a GPU)
+    prints one JSON line with the contract keys the driver reads."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HRT_REF_SENTENCES="1")
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1"], capture_output=True, text=True, env=env, timeout=600, cwd=repo)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
