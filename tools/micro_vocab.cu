@@ -92,11 +92,11 @@ int main() {
   for (int M : {1, 8}) {
     for (int rep = 0; rep < 2; ++rep) {
       for (int w = 0; w < 5; ++w)
-        gemv_vocab_kernel<1, false><<<nt, GV_THREADS>>>(A, K, E, V, K, M, nullptr, p, 0, GvLN{nullptr, nullptr, nullptr});
+        gemv_vocab_kernel<1, false><<<nt, GV_VWARPS * 32>>>(A, K, E, V, K, M, nullptr, p, 0, GvLN{nullptr, nullptr, nullptr});
       cudaEventRecord(a);
       const int it = 200;
       for (int w = 0; w < it; ++w)
-        gemv_vocab_kernel<1, false><<<nt, GV_THREADS>>>(A, K, E, V, K, M, nullptr, p, 0, GvLN{nullptr, nullptr, nullptr});
+        gemv_vocab_kernel<1, false><<<nt, GV_VWARPS * 32>>>(A, K, E, V, K, M, nullptr, p, 0, GvLN{nullptr, nullptr, nullptr});
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
