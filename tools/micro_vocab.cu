@@ -122,8 +122,8 @@ int main() {
     float* o;
     cudaMalloc(&o, 4096);
     auto go = [&]() {
-      if (nb == 8) pattern_kernel<8><<<nt, 512>>>(E, V, K, o);
-      else pattern_kernel<16><<<nt, 512>>>(E, V, K, o);
+      if (nb == 8) pattern_kernel<8><<<nt, GV_VWARPS * 32>>>(E, V, K, o);
+      else pattern_kernel<16><<<nt, GV_VWARPS * 32>>>(E, V, K, o);
     };
     for (int w = 0; w < 5; ++w) go();
     cudaEventRecord(a);
@@ -138,8 +138,8 @@ int main() {
     float* o;
     cudaMalloc(&o, 4096);
     auto go = [&]() {
-      if (nb == 8) native_kernel<8><<<nt, 512>>>(E, V, K, o);
-      else native_kernel<16><<<nt, 512>>>(E, V, K, o);
+      if (nb == 8) native_kernel<8><<<nt, GV_VWARPS * 32>>>(E, V, K, o);
+      else native_kernel<16><<<nt, GV_VWARPS * 32>>>(E, V, K, o);
     };
     for (int w = 0; w < 5; ++w) go();
     cudaEventRecord(a);
