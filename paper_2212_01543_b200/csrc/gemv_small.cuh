@@ -231,6 +231,23 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
     u1[i] = gv_ldw(wf + (size_t)(2 * ch + 1) * 256, pol);
   }
   pdl_wait();
+  // Activation fragments do not depend on the live row count: for the small
+  // shapes they are requested before the device row count resolves (rows
+  // clamped to the launch's host bound, which the buffer always holds; rows
+  // past the live count are computed and discarded) -- one dependent round
+  // trip fewer on the critical path.
+  constexpr bool HOIST = !LNA && CPW * NT <= 8;
+  uint4 av[HOIST ? CPW : 1][HOIST ? NT : 1];
+  if constexpr (HOIST) {
+    const int m_host = M;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        av[i][j] = c0 + i < c1 ? *reinterpret_cast<const uint4*>(A + (size_t)min(8 * j + g, m_host - 1) * lda +
+                                                                  32 * (c0 + i) + t4 * 8)
+                               : make_uint4(0, 0, 0, 0);
+  }
   if (M_dev) M = *M_dev;
   // The final reduction and epilogue are spread over NG warps: warp w < NG owns
   // n-tiles w, w + NG, ...; its epilogue operands (residual rows, bias) are
@@ -267,8 +284,13 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         if (j < nt_live) {
-          const int r = min(8 * j + g, M - 1);
-          const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (c0 + i) + t4 * 8);
+          uint4 v;
+          if constexpr (HOIST) {
+            v = av[i][j];
+          } else {
+            const int r = min(8 * j + g, M - 1);
+            v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (c0 + i) + t4 * 8);
+          }
           gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
           gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
         }
