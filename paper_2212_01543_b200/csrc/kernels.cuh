@@ -46,22 +46,29 @@ template <typename T, int NV>
 __global__ void layernorm_vec_kernel(const float* __restrict__ x, const int* __restrict__ M_dev, int M, int d,
                                      const float* __restrict__ g, const float* __restrict__ b, T* __restrict__ y,
                                      const int* __restrict__ out_row, float* __restrict__ y32) {
-  pdl_enter();
-  if (M_dev) M = *M_dev;
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const int orow = out_row ? out_row[row] : row;
-  if (orow < 0) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
-  float4 v[NV], gv[NV], bv[NV];  // gain / bias loads issued with the row (one round trip)
-  float s = 0.f;
+  float4 v[NV], gv[NV], bv[NV];
+  // gain / bias never change: requested before the grid-dependency wait
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    v[i] = xr[lane + 32 * i];
     gv[i] = __ldg(reinterpret_cast<const float4*>(g) + lane + 32 * i);
     bv[i] = __ldg(reinterpret_cast<const float4*>(b) + lane + 32 * i);
   }
+  pdl_wait();
+  // the row is requested before the device row count resolves (clamped to the
+  // launch's host bound, which the buffer always holds)
+  {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)min(row, M - 1) * d);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+  }
+  if (M_dev) M = *M_dev;
+  if (row >= M) return;
+  const int orow = out_row ? out_row[row] : row;
+  if (orow < 0) return;
+  float s = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   const float mean = warp_sum(s) / d;
