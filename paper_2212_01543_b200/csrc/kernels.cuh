@@ -911,15 +911,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   }
   pdl_wait();
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;
-  if (R_dev) R = *R_dev;
-  if (t_dev) t = *t_dev;
-  // beam decoding ping-pongs the history map by step parity (reorder writes the other one)
-  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;  // nullptr: identity
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * nwarp + warp;
-  if (item >= R * heads) return;
-  const int r = item / heads, h = item - r * heads;
-  float* sc = sm + warp * lk_max;
+  // the query row is requested before the device row count / step resolve
+  // (row clamped to the launch's host bound; items past the live rows exit below)
+  const int r = min(item / heads, R - 1), h = item - (item / heads) * heads;
   const int hoff = h * DH;
   float qr[DH];
   {
@@ -934,6 +930,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
 #pragma unroll
     for (int c = 0; c < DH; ++c) qr[c] *= scale;
   }
+  if (R_dev) R = *R_dev;
+  if (t_dev) t = *t_dev;
+  if (item >= R * heads) return;
+  // beam decoding ping-pongs the history map by step parity (reorder writes the other one)
+  const int* __restrict__ hist = (hist_b != nullptr && (t & 1)) ? hist_b : hist_a;  // nullptr: identity
+  float* sc = sm + warp * lk_max;
   int L;
   size_t kv_row0 = 0;
   if (SELF) {
