@@ -1551,19 +1551,25 @@ __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restri
 template <typename T, int KT>
 __global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, int k, StepCtl* ctl) {
   pdl_enter();
-  if (ctl) {
-    R = ctl->R;
-    t = ctl->t;
-    k = ctl->k;
-  }
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  // the row's partials, done flag and the step control are requested together
+  // (row clamped to the launch's host bound; rows past the live count exit below)
+  const int rr = min(row, R - 1);
+  StepCtl c{};
+  if (ctl) c = *ctl;
+  const int done_v = st.done[rr];
+  const RowStat rs = KT == 1 ? merge_row1(parts, rr) : merge_row<KT>(parts, rr, 1);
+  if (ctl) {
+    R = c.R;
+    t = c.t;
+    k = c.k;
+  }
   if (row >= R) return;
   int tok;
-  if (st.done[row]) {
+  if (done_v) {
     tok = st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
   } else {
-    const RowStat rs = KT == 1 ? merge_row1(parts, row) : merge_row<KT>(parts, row, 1);
     tok = 0;
     if (lane == 0) {
       const bool last = (t == st.caps[row] - 1);
