@@ -404,6 +404,15 @@ __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* 
     u1[i] = gv_ldw(wf + (size_t)(2 * ch + 1) * 256, pol);
   }
   pdl_wait();
+  // NT = 1: the first batch of activation fragments is requested before the
+  // device row count resolves (row clamped to the launch's host bound)
+  constexpr bool HOIST = NT == 1 && !LNA;
+  uint4 a0[HOIST ? GV_MAXC : 1];
+  if constexpr (HOIST) {
+    const bf16* ar = A + (size_t)min(g, M - 1) * lda + t4 * 8;
+#pragma unroll
+    for (int i = 0; i < GV_MAXC; ++i) a0[i] = *reinterpret_cast<const uint4*>(ar + 32 * min(i, nch - 1));
+  }
   if (M_dev) M = *M_dev;
   if (LNA) {
     gv_ln_stats(ln, M, K, lnst);
@@ -421,7 +430,12 @@ __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* 
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int r = min(8 * j + g, M - 1);
-          const uint4 v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (cb + i) + t4 * 8);
+          uint4 v;
+          if constexpr (HOIST) {
+            v = cb == 0 ? a0[i] : gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (cb + i) + t4 * 8);
+          } else {
+            v = gv_afrag<LNA>(A, lda, ln, lnst, K, r, 32 * (cb + i) + t4 * 8);
+          }
           gv_mma(c[j], u0[i].x, u1[i].x, u0[i].y, u1[i].y, v.x, v.y);
           gv_mma(c[j], u0[i].z, u1[i].z, u0[i].w, u1[i].w, v.z, v.w);
         }
