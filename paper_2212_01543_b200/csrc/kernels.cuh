@@ -761,6 +761,15 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
     pre = true;
   }
   pdl_wait();
+  // the query row is requested before the device row count / step resolve (the
+  // grid never exceeds the launch's host bound, which the buffer holds)
+  constexpr int QPT = (d + 63) / 64;  // >= d / blockDim.x for blockDim.x >= 64
+  float qv[QPT];
+#pragma unroll
+  for (int i = 0; i < QPT; ++i) {
+    const int c = tid + i * nthr;
+    qv[i] = c < d ? to_f(q[(size_t)r * q_stride + c]) * scale : 0.f;
+  }
   if (R_dev) R = *R_dev;
   if (t_dev) t = *t_dev;
   if (r >= R) {
@@ -784,7 +793,11 @@ __global__ void __launch_bounds__(512) attn_decode_rows_kernel(
     L = kv_len[sq];
     kv_row0 = kv_off[sq];
   }
-  for (int c = tid; c < d; c += nthr) qs[c] = to_f(q[(size_t)r * q_stride + c]) * scale;
+#pragma unroll
+  for (int i = 0; i < QPT; ++i) {
+    const int c = tid + i * nthr;
+    if (c < d) qs[c] = qv[i];
+  }
   const int h = warp;
   const bool active = h < heads_c;
   float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f;
