@@ -63,8 +63,8 @@ typedef struct hrt_engine hrt_engine;
 typedef struct hrt_stats {
   int64_t kernel_launches;   /* kernels this engine launched (all calls) */
   int64_t decoder_calls;     /* reference decoder-call counter (infer.py:161) */
-  int64_t arena_bytes;       /* device activation arena capacity */
-  int64_t arena_high_water;  /* largest phase footprint seen */
+  int64_t arena_bytes;       /* device activation arena capacity (hrt_estimate_arena max) */
+  int64_t arena_high_water;  /* largest phase footprint any call needed (<= arena_bytes) */
   int64_t weight_bytes;      /* device weight blob */
 } hrt_stats;
 
@@ -77,6 +77,11 @@ hrt_status hrt_create(const hrt_config* cfg, const float* params, int64_t n_para
 void hrt_destroy(hrt_engine* eng);
 int64_t hrt_param_count(const hrt_config* cfg);
 const char* hrt_last_error(const hrt_engine* eng);  /* eng may be NULL: last global error */
+/* Closed-form activation-arena bytes per phase for an engine of this config
+ * (estimate_max_bytes, infer.py:78-96): phase_bytes[0] encoder, [1] skip-AT
+ * (Stage I), [2] skip-CMLM (Stage II), [3] max = the arena capacity that
+ * hrt_create allocates. Phases alias one allocation. No GPU needed. */
+hrt_status hrt_estimate_arena(const hrt_config* cfg, int64_t* phase_bytes);
 hrt_status hrt_get_stats(const hrt_engine* eng, hrt_stats* out);
 void* hrt_stream(hrt_engine* eng);                  /* the engine's cudaStream_t */
 hrt_status hrt_synchronize(hrt_engine* eng);
@@ -114,6 +119,9 @@ typedef struct hrt_translate_out {
 } hrt_translate_out;
 
 /* Translate B sentences. ids: packed source tokens (sum(lens) entries);
+ * sources longer than max_len keep their first max_len tokens (decoding.py:260);
+ * host ids outside [0, vocab_size) fail with HRT_ERR_INVALID (np.take's
+ * IndexError), device-resident ids (io_on_device 1) are clamped to EOS;
  * lens and max_steps are HOST arrays (the schedule); max_steps NULL means the
  * reference default ceil(max_len / k) (decoding.py:202-203). When
  * io_on_device is 0, ids and every output pointer are host memory and the
@@ -124,6 +132,15 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
                                int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
                                const hrt_translate_out* out, int32_t io_on_device);
 
+/* Autoregressive baseline (decoding.at_translate, decoding.py:163-185) on the
+ * same kernels and captured Stage-I loop: interval 1 from BOS, no Stage II.
+ * Greedy only (beam must be 1; AT beam search runs through the session
+ * protocol). max_steps NULL means max_len steps. Outputs as for
+ * hrt_translate_batch: scores = {s, 0, s / len^length_penalty}, calls = steps. */
+hrt_status hrt_at_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t B, int32_t beam,
+                                  float length_penalty, const int32_t* max_steps, const hrt_translate_out* out,
+                                  int32_t io_on_device);
+
 /* Engine options (speed only; "graphs", "graph_unroll", "cluster" are bit-identical, the kernel-path
  * switches change the bf16 summation order):
  *   "graphs"        1 (default): Stage-I steps replayed from captured CUDA graphs; 0: launched step by step
@@ -131,13 +148,10 @@ hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_
  *                   WHILE-node graph per row bucket (the original design, measured slower)
  *   "cluster"       1 (default): large-M tcgen05 GEMMs as CTA pairs sharing the weight tile
  *   "gemv", "gemv_max_m", "bn32", "attn_heads", "attn_rows", "splitk", "ln_fuse", "tail_ln",
- *   "l2_persist", "mega": kernel-path switches documented in DESIGN.md §4 / §7. */
+ *   "l2_persist": kernel-path switches documented in DESIGN.md §4 / §7. */
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
 
 /* ---- measurement helpers ------------------------------------------------ */
-/* Debug: globaltimer stamps (ns) at each phase barrier of the first tail-megakernel
- * step of the last call (option "mega_trace" must be on); up to 64 entries. */
-hrt_status hrt_debug_trace(hrt_engine* eng, int64_t* out, int32_t n);
 /* Kernel-class timing: when enabled, CUDA events bracket every launch of the
  * named class ("vocab", "gemm", "attn", "all") on the engine stream. */
 hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable);

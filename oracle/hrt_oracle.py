@@ -511,3 +511,81 @@ def at_translate(sess: Oracle, source, beam=1, length_penalty=0.6, max_len=None)
         forced=best.forced,
         anchors=list(best.tokens),
     )
+
+
+# ---------------------------------------------------------------------------
+# parity accounting (SURVEY §8(c) protocol, steps 3-4): teacher-forced
+# agreement with top-2 margins. Not part of the reference; built from its
+# own pieces -- Stage-I rows come from a causal parallel_logits pass over the
+# anchor prefix, which equals incremental `step` (test_acceptance.py:211-231),
+# and Stage-II rows from the full pass of decoding.py:268-285.
+# ---------------------------------------------------------------------------
+
+
+def _top2_margin(row):
+    """(argmax, top1 - top2) of a logits / log-prob row over the allowed set."""
+    r = allowed_row(row)
+    i = int(np.argmax(r))
+    top1 = r[i]
+    r[i] = -np.inf
+    return i, float(top1 - r.max())
+
+
+def greedy_teacher_forced(sess: Oracle, source, k, tokens, max_steps, tie=1e-3):
+    """Score an engine's greedy HRT output against the oracle, position by
+    position, with the engine's own prefix fed to the oracle (so one flip does
+    not cascade). `tokens` is the engine's Translation.tokens.
+
+    Returns counts: s1 / s2 positions compared, agreements, and near-ties
+    (positions whose oracle top-2 margin is below `tie`), plus `bad`, the
+    disagreements that are NOT near-ties (must be 0 for an exact fp32 path).
+    Stage II is compared only when the anchors can be read back from `tokens`
+    (no EOS fill truncated the output).
+    """
+    c = sess.cfg
+    out = dict(s1=0, s1_agree=0, s1_ties=0, s2=0, s2_agree=0, s2_ties=0, bad=0)
+    sess.encode(list(source)[: c.max_len])
+    tokens = list(tokens)
+    n = len(tokens)
+    complete = (n + 1) % k == 0 and (n + 1) // k <= max_steps
+    anchors = tokens[k - 1:: k] + ([EOS] if complete else [])
+    if not anchors:
+        return out
+    m = len(anchors)
+    feed = [BOS_K[k]] + anchors[: m - 1]
+    logits = sess.parallel_logits([feed], [[t * k for t in range(m)]], "causal")[0]
+    for t in range(m):
+        if t == max_steps - 1:  # forced EOS at the cap (decoding.py:108)
+            continue
+        if not complete and t == m - 1 and anchors[t] == EOS:
+            continue
+        am, margin = _top2_margin(logits[t])
+        out["s1"] += 1
+        if am == anchors[t]:
+            out["s1_agree"] += 1
+        elif margin < tie:
+            out["s1_ties"] += 1
+        else:
+            out["bad"] += 1
+    if not complete:
+        return out
+    ids, pos = build_stage2_input(anchors, k)
+    logits = sess.parallel_logits([ids], [pos], "full")[0]
+    filled = tokens + [EOS]
+    for j, tok in enumerate(ids):
+        if tok != MASK or j >= len(filled):
+            continue
+        am, margin = _top2_margin(logits[j])
+        out["s2"] += 1
+        if am == filled[j]:
+            out["s2_agree"] += 1
+        elif margin < tie:
+            out["s2_ties"] += 1
+        else:
+            out["bad"] += 1
+    return out
+
+
+def free_running_agreement(a, b):
+    """Positional token agreement of two decodes: (agreeing positions, max length)."""
+    return sum(x == y for x, y in zip(a, b)), max(len(a), len(b))

@@ -18,9 +18,9 @@ HRT_DTYPE_F32, HRT_DTYPE_BF16 = 0, 1
 
 # every symbol include/hrt_b200.h declares
 EXPORTED = (
-    "hrt_create", "hrt_destroy", "hrt_param_count", "hrt_last_error", "hrt_get_stats", "hrt_stream",
+    "hrt_create", "hrt_destroy", "hrt_param_count", "hrt_estimate_arena", "hrt_last_error", "hrt_get_stats", "hrt_stream",
     "hrt_synchronize", "hrt_encode", "hrt_start_cache", "hrt_step", "hrt_reorder", "hrt_parallel_logits",
-    "hrt_argmax_logprobs", "hrt_translate_batch", "hrt_set_option", "hrt_phase_times", "hrt_debug_trace", "hrt_timing_enable",
+    "hrt_argmax_logprobs", "hrt_translate_batch", "hrt_at_translate_batch", "hrt_set_option", "hrt_phase_times", "hrt_timing_enable",
     "hrt_timing_report", "hrt_timing_read",
 )
 
@@ -63,6 +63,7 @@ def load(path: str | None = None):
         "hrt_create": ([C.POINTER(HrtConfig), f32p, i64, i32, C.POINTER(vp)], C.c_int),
         "hrt_destroy": ([vp], None),
         "hrt_param_count": ([C.POINTER(HrtConfig)], i64),
+        "hrt_estimate_arena": ([C.POINTER(HrtConfig), C.POINTER(C.c_int64)], C.c_int),
         "hrt_last_error": ([vp], C.c_char_p),
         "hrt_get_stats": ([vp, C.POINTER(HrtStats)], C.c_int),
         "hrt_stream": ([vp], vp),
@@ -75,9 +76,10 @@ def load(path: str | None = None):
         "hrt_argmax_logprobs": ([vp, i32p, i32, i32p, f32p], C.c_int),
         "hrt_translate_batch": ([vp, vp, i32p, i32, i32, i32, i32, C.c_float, i32p,
                                  C.POINTER(HrtTranslateOut), i32], C.c_int),
+        "hrt_at_translate_batch": ([vp, vp, i32p, i32, i32, C.c_float, i32p, C.POINTER(HrtTranslateOut), i32],
+                                   C.c_int),
         "hrt_set_option": ([vp, C.c_char_p, i32], C.c_int),
         "hrt_phase_times": ([vp, f32p], C.c_int),
-        "hrt_debug_trace": ([vp, C.POINTER(C.c_int64), i32], C.c_int),
         "hrt_timing_report": ([vp, C.c_char_p, i64], C.c_int),
         "hrt_timing_enable": ([vp, C.c_char_p, i32], C.c_int),
         "hrt_timing_read": ([vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),

@@ -26,29 +26,13 @@
 #include "gemm_simt.cuh"
 #include "gemv_small.cuh"
 #include "kernels.cuh"
-#include "decode_mega.cuh"
 #include "tc_gemm.cuh"
 #include "tmap.h"
 
+#include "engine_iface.h"
+
 namespace hrt {
-
-struct HrtError : std::runtime_error {
-  hrt_status code;
-  HrtError(hrt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-#define CUDA_OK(x)                                                                                     \
-  do {                                                                                                 \
-    cudaError_t _e = (x);                                                                              \
-    if (_e != cudaSuccess)                                                                             \
-      throw HrtError(HRT_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " @" + \
-                                       std::to_string(__LINE__));                                      \
-  } while (0)
-
-static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
-static inline size_t align_up(size_t n, size_t a = 256) { return (n + a - 1) / a * a; }
-
-enum KClass { K_GEMM = 1, K_VOCAB = 2, K_ATTN = 4, K_OTHER = 8 };
+using namespace hrtcore;
 
 // ---------------------------------------------------------------------------
 // Device arena: one allocation, per-phase buffer plans carved at fixed
@@ -65,136 +49,6 @@ struct Plan {
   }
 };
 
-// ---------------------------------------------------------------------------
-// engine
-// ---------------------------------------------------------------------------
-struct EngineBase {
-  hrt_config cfg{};
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  std::string last_error;
-  hrt_stats stats{};
-  // phase timing: events at the phase boundaries of the last fused call
-  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool phase_valid = false;
-  void phase_mark(int i) {
-    if (!phase_ev[i]) cudaEventCreate(&phase_ev[i]);
-    cudaEventRecord(phase_ev[i], stream);
-  }
-  // kernel-class timing
-  int timed_class = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
-  std::vector<const char*> ev_tag;
-  std::vector<double> ev_flops;  // algorithmic FLOPs of each timed launch
-  size_t ev_used = 0;
-  const char* cur_tag = "untagged";  // call-site tag for the next launches
-  double t_bytes = 0, t_flops = 0;
-  int64_t t_launches = 0;
-
-  virtual ~EngineBase() {
-    for (auto& p : ev_pool) {
-      cudaEventDestroy(p.first);
-      cudaEventDestroy(p.second);
-    }
-    if (stream) cudaStreamDestroy(stream);
-  }
-  virtual void encode(const int32_t* ids, const int32_t* lens, int n, float* mem_out) = 0;
-  virtual void start_cache(int rows, int cap, const int32_t* row_seq) = 0;
-  virtual void step(const int32_t* tokens, int position, float* logp_out) = 0;
-  virtual void reorder(const int32_t* parents) = 0;
-  virtual void parallel_logits(const int32_t* ids, const int32_t* pos, const uint8_t* pad, int B, int T, int mode,
-                               const int32_t* seq, float* logits_out) = 0;
-  virtual void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) = 0;
-  virtual void set_option(const std::string& name, int value) = 0;
-  virtual void debug_trace(int64_t* out, int n) = 0;
-  virtual void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
-                         const int32_t* caps, const hrt_translate_out* out, int on_device) = 0;
-
-  // --- launch bookkeeping -------------------------------------------------
-  struct Scope {
-    EngineBase* e;
-    std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
-    Scope(EngineBase* eng, int cls, double bytes, double flops) : e(eng) {
-      if (e->timed_class & cls) {
-        if (e->ev_used == e->ev_pool.size()) {
-          cudaEvent_t a, b;
-          cudaEventCreate(&a);
-          cudaEventCreate(&b);
-          e->ev_pool.emplace_back(a, b);
-        }
-        if (e->ev_tag.size() < e->ev_pool.size()) e->ev_tag.resize(e->ev_pool.size());
-        if (e->ev_flops.size() < e->ev_pool.size()) e->ev_flops.resize(e->ev_pool.size());
-        e->ev_tag[e->ev_used] = e->cur_tag;
-        e->ev_flops[e->ev_used] = flops;
-        ev = &e->ev_pool[e->ev_used++];
-        cudaEventRecord(ev->first, e->stream);
-        e->t_bytes += bytes;
-        e->t_flops += flops;
-        e->t_launches += 1;
-      }
-    }
-    ~Scope() {
-      if (ev) cudaEventRecord(ev->second, e->stream);
-      e->stats.kernel_launches += 1;
-    }
-  };
-  bool pdl = true;  // programmatic dependent launch on every kernel
-  // dynamic shared-memory opt-in per kernel (process-wide: kernels of one
-  // signature share a generic lambda's statics, so the key is the function)
-  template <class K>
-  static void smem_optin(K kern, size_t bytes) {
-    static std::map<const void*, size_t> done;
-    size_t& have = done[reinterpret_cast<const void*>(kern)];
-    if (have >= bytes) return;
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    have = bytes;
-  }
-  int launch_cluster = 1;  // cluster size of the next launch (set by tc_launch only)
-  template <typename... KArgs, typename... Args>
-  void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (pdl) {
-      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[na].val.programmaticStreamSerializationAllowed = 1;
-      ++na;
-    }
-    if (launch_cluster > 1) {  // thread-block clusters along x (tcgen05 GEMM CTA pairs)
-      attr[na].id = cudaLaunchAttributeClusterDimension;
-      attr[na].val.clusterDim.x = launch_cluster;
-      attr[na].val.clusterDim.y = 1;
-      attr[na].val.clusterDim.z = 1;
-      ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    cudaError_t er = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-    if (er != cudaSuccess) {
-      const char* fname = nullptr;
-      if (cudaFuncGetName(&fname, reinterpret_cast<const void*>(kern)) != cudaSuccess) fname = "?";
-      throw HrtError(HRT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(er) + " (" + fname + ", grid " +
-                                       std::to_string(grid.x) + "x" + std::to_string(grid.y) + ", block " +
-                                       std::to_string(block.x) + ", smem " + std::to_string(smem) + ", cluster " +
-                                       std::to_string(launch_cluster) + ")");
-    }
-  }
-  struct Tag {
-    EngineBase* e;
-    const char* prev;
-    Tag(EngineBase* eng, const char* t) : e(eng), prev(eng->cur_tag) { e->cur_tag = t; }
-    ~Tag() { e->cur_tag = prev; }
-  };
-  void check_launch() {
-    cudaError_t er = cudaGetLastError();
-    if (er != cudaSuccess) throw HrtError(HRT_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(er));
-  }
-};
 
 template <typename T>
 struct Engine : EngineBase {
@@ -252,15 +106,6 @@ struct Engine : EngineBase {
   int debug_spin_us = 0;
   int enc_skip = 0;  // option "enc_skip" (debug attribution of the encoder kernels)  // option "debug_spin" (host-bound vs device-bound attribution)
   bool greedy_hist_identity = false;  // set during greedy Stage I: history map is the identity
-  bool use_mega = false;  // option "mega": Stage-I steps with <= MG_RMAX live rows in the persistent decode kernel (measured ~parity with the graph path at B=1; off by default)
-  bf16 *mg_q = nullptr, *mg_ctx = nullptr, *mg_hid = nullptr;
-  float4* mg_vpart = nullptr;
-  float* mg_veos = nullptr;
-  int mg_trace_step = 1;
-  int mg_skip = 0;  // debug option mega_skip (timing attribution only)
-  unsigned* mg_bar = nullptr;
-  unsigned long long* mg_trace = nullptr;  // debug option "mega_trace"
-  bool mg_trace_on = false;
   // debug: drop kernel groups from the Stage-I step (timing attribution only;
   // results are meaningless when nonzero). 1 LN, 2 attention, 4 GEMMs,
   // 8 vocab, 16 select, 32 embed.
@@ -352,12 +197,6 @@ struct Engine : EngineBase {
     cudaFree(sk_ws);
     cudaFree(sk_counters);
     cudaFree(gv_counter);
-    cudaFree(mg_q);
-    cudaFree(mg_ctx);
-    cudaFree(mg_hid);
-    cudaFree(mg_vpart);
-    cudaFree(mg_veos);
-    cudaFree(mg_bar);
     if (h_meta) cudaFreeHost(h_meta);
     if (h_out) cudaFreeHost(h_out);
     drop_loop_graphs();
@@ -618,16 +457,35 @@ struct Engine : EngineBase {
   // -------------------------------------------------------------------------
   // capacity + arena plan
   // -------------------------------------------------------------------------
+  // Arena dimensions: the engine's capacity (max_dims), or one call's actual
+  // sizes when accounting the high-water mark. One closed form serves the
+  // allocation, the high-water mark and hrt_estimate_arena (estimate_max_bytes,
+  // infer.py:78-96).
+  struct ArenaDims {
+    int Me, R, M2, Mm;
+  };
+  static ArenaDims max_dims(const hrt_config& c) {
+    const int B = std::max(1, c.max_sentences), beam = std::max(1, c.max_beam);
+    const int M2 = B * beam * (c.max_len + c.max_chunk);
+    return ArenaDims{c.max_src_tokens > 0 ? c.max_src_tokens : B * c.max_len, B * beam, M2, M2};
+  }
   void size_capacity() {
+    const ArenaDims a = max_dims(cfg);
     Bmax = std::max(1, cfg.max_sentences);
     beam_max = std::max(1, cfg.max_beam);
-    Me_max = cfg.max_src_tokens > 0 ? cfg.max_src_tokens : Bmax * Lmax;
-    R_max = Bmax * beam_max;
+    Me_max = a.Me;
+    R_max = a.R;
     cap_max = Lmax + 1;  // AT mode (k = 1) worst case; skip-AT needs ceil(L/k)+1
-    M2_max = Bmax * beam_max * (Lmax + cfg.max_chunk);
-    Mm_max = M2_max;
+    M2_max = a.M2;
+    Mm_max = a.Mm;
     nt_max = cdiv(V, 64);
     logit_rows = 4096;
+  }
+  // largest phase footprint of a call with these sizes (arena_high_water)
+  void note_high_water(int phase, const ArenaDims& a) {
+    Plan p;
+    carve_plan(phase, p, nullptr, a, cfg, nullptr);
+    stats.arena_high_water = std::max<int64_t>(stats.arena_high_water, (int64_t)p.off);
   }
 
   template <class Fn>
@@ -645,9 +503,31 @@ struct Engine : EngineBase {
   // partials per row for the selection merge, one tile per CTA at small R)
   int vocab_bn(int rows) const { return V >= 4096 ? 256 : std::max(64, choose_bn(rows, V)); }  // row-wise epilogue: column halves
   // upper bound on vocab tiles per row for any row count (partials sizing)
-  int nt_bound() const { return (BF16 && V < 4096) ? cdiv(V, 32) : cdiv(V, 128); }
+  static int nt_bound(const hrt_config& c) {
+    return (BF16 && c.vocab_size < 4096) ? cdiv(c.vocab_size, 32) : cdiv(c.vocab_size, 128);
+  }
+  static void estimate(const hrt_config& c, int64_t* phase_bytes) {
+    const ArenaDims a = max_dims(c);
+    int64_t mx = 0;
+    for (int ph = 0; ph < 3; ++ph) {
+      Plan p;
+      carve_plan(ph, p, nullptr, a, c, nullptr);
+      phase_bytes[ph] = (int64_t)p.off;
+      mx = std::max(mx, phase_bytes[ph]);
+    }
+    phase_bytes[3] = mx;
+  }
 
-  void carve(int phase, Plan& p, char* base) {
+  static void carve_plan(int phase, Plan& p, char* base, const ArenaDims& a, const hrt_config& c, Engine* e) {
+    const int d = c.d_model, ff = c.d_ff, Ld = c.dec_layers, V = c.vocab_size, cap_max = c.max_len + 1;
+    const int logit_rows = 4096;
+    const int Me_max = a.Me, R_max = a.R, M2_max = a.M2, Mm_max = a.Mm;
+    EncBufs eb_{};
+    S1Bufs s1_{};
+    S2Bufs s2_{};
+    EncBufs& eb = e ? e->eb : eb_;
+    S1Bufs& s1 = e ? e->s1 : s1_;
+    S2Bufs& s2 = e ? e->s2 : s2_;
     if (phase == 0) {
       eb.x = p.take<float>(base, (size_t)Me_max * d);
       eb.y = p.take<T>(base, (size_t)Me_max * d);
@@ -663,7 +543,7 @@ struct Engine : EngineBase {
       s1.hid = p.take<T>(base, (size_t)R_max * ff);
       s1.kc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
       s1.vc = p.take<T>(base, (size_t)Ld * R_max * cap_max * d);
-      const size_t ntot = (size_t)R_max * nt_bound();
+      const size_t ntot = (size_t)R_max * nt_bound(c);
       s1.parts.mx = p.take<float>(base, ntot);
       s1.parts.sum = p.take<float>(base, ntot);
       s1.parts.val = p.take<float>(base, ntot * KTOP_MAX);
@@ -682,7 +562,7 @@ struct Engine : EngineBase {
       s2.ids = p.take<int>(base, M2_max);
       s2.pos = p.take<int>(base, M2_max);
       s2.out_row = p.take<int>(base, M2_max);
-      const size_t ntot = (size_t)Mm_max * nt_bound();
+      const size_t ntot = (size_t)Mm_max * nt_bound(c);
       s2.parts.mx = p.take<float>(base, ntot);
       s2.parts.sum = p.take<float>(base, ntot);
       s2.parts.val = p.take<float>(base, ntot);  // KT = 1 in Stage II
@@ -695,7 +575,7 @@ struct Engine : EngineBase {
 
   void alloc_buffers() {
     // persistent region
-    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256 + 8 + 2 * (cap_max + 8) + 2 * (Bmax + 16) +
+    meta_cap = 16 * Bmax * beam_max + 10 * M2_max + 2 * V + 256 + 8 + 2 * (cap_max + 8) + 2 * (R_max + 16) +
                Me_max + Bmax + 8;  // + the call's source ids
     auto persist_plan = [&](char* base) {
       Plan p;
@@ -741,17 +621,21 @@ struct Engine : EngineBase {
     size_t pbytes = persist_plan(nullptr);
     CUDA_OK(cudaMalloc(&persist, pbytes));
     persist_plan(persist);
+    CUDA_OK(cudaMemset(persist, 0, pbytes));
     // fixed header of the metadata buffer: Stage-I loop control, alive[],
     // source offsets / lengths (graph-captured kernels keep these pointers)
-    meta_hdr = 8 + align_up(cap_max + 1, 8) + align_up(Bmax + 1, 8) + align_up(Bmax, 8);
+    // source offsets / lengths are sized for R_max rows: graph launches cover a
+    // power-of-two row bucket, and rows past the live sentences read length 0
+    meta_hdr = 8 + align_up(cap_max + 1, 8) + align_up(R_max + 1, 8) + align_up(R_max, 8);
     s_ctl = reinterpret_cast<StepCtl*>(d_meta);
     s_alive = d_meta + 8;
     s_srcoff = s_alive + align_up(cap_max + 1, 8);
-    s_srclen = s_srcoff + align_up(Bmax + 1, 8);
+    s_srclen = s_srcoff + align_up(R_max + 1, 8);
     arena_bytes = 0;
+    const ArenaDims amax = max_dims(cfg);
     for (int ph = 0; ph < 3; ++ph) {
       Plan p;
-      carve(ph, p, nullptr);
+      carve_plan(ph, p, nullptr, amax, cfg, this);
       arena_bytes = std::max(arena_bytes, p.off);
     }
     cudaError_t e = cudaMalloc(&arena, arena_bytes);
@@ -762,17 +646,13 @@ struct Engine : EngineBase {
     }
     for (int ph = 0; ph < 3; ++ph) {
       Plan p;
-      carve(ph, p, arena);
+      carve_plan(ph, p, arena, amax, cfg, this);
     }
-    stats.arena_bytes = (int64_t)(arena_bytes + pbytes);
+    // the activation arena (phases alias); the persistent handoff region (cross-K/V,
+    // Stage-I state, I/O staging) lives outside it, like the reference session's
+    // memory / cross_k / cross_v (infer.py:156-160)
+    stats.arena_bytes = (int64_t)arena_bytes;
     if (BF16) {
-      CUDA_OK(cudaMalloc(&mg_q, (size_t)MG_RMAX * d * sizeof(bf16)));
-      CUDA_OK(cudaMalloc(&mg_ctx, (size_t)MG_RMAX * d * sizeof(bf16)));
-      CUDA_OK(cudaMalloc(&mg_hid, (size_t)MG_RMAX * ff * sizeof(bf16)));
-      CUDA_OK(cudaMalloc(&mg_vpart, (size_t)MG_RMAX * num_sms * sizeof(float4)));
-      CUDA_OK(cudaMalloc(&mg_veos, MG_RMAX * sizeof(float)));
-      CUDA_OK(cudaMalloc(&mg_bar, 2 * sizeof(unsigned)));
-      CUDA_OK(cudaMemset(mg_bar, 0, 2 * sizeof(unsigned)));
       CUDA_OK(cudaMalloc(&sk_ws, sk_ws_bytes));
       CUDA_OK(cudaMalloc(&sk_counters, sk_max_tiles * sizeof(int)));
       CUDA_OK(cudaMemset(sk_counters, 0, sk_max_tiles * sizeof(int)));
@@ -1435,7 +1315,8 @@ struct Engine : EngineBase {
   // session protocol
   // -------------------------------------------------------------------------
   void encode(const int32_t* ids, const int32_t* lens, int n, float* mem_out) override {
-    if (n < 1 || n > Bmax) throw HrtError(HRT_ERR_INVALID, "n_seq out of range");
+    if (n < 1) throw HrtError(HRT_ERR_INVALID, "n_seq out of range");
+    if (n > Bmax) throw HrtError(HRT_ERR_MEMORY, "n_seq exceeds the arena's max_sentences");
     std::vector<int> off(n + 1, 0), len(n);
     int maxl = 0;
     for (int i = 0; i < n; ++i) {
@@ -1449,6 +1330,8 @@ struct Engine : EngineBase {
     }
     const int M = off[n];
     if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed capacity");
+    for (int i = 0; i < M; ++i)
+      if (ids[i] < 0 || ids[i] >= V) throw HrtError(HRT_ERR_INVALID, "source token id out of range");
     std::vector<int> pos(M);
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < len[i]; ++j) pos[off[i] + j] = j;
@@ -1474,6 +1357,7 @@ struct Engine : EngineBase {
       p_mem_target = p_mem;
     }
     run_encoder(M, n, maxl, d_off, d_len, d_items, (int)items.size() / 2);
+    note_high_water(0, ArenaDims{M, 0, 0, 0});
     p_mem_target = nullptr;
     if (Le == 0 && mem_out) throw HrtError(HRT_ERR_INVALID, "memory output needs enc_layers >= 1");
     if (mem_out) {
@@ -1494,10 +1378,12 @@ struct Engine : EngineBase {
   std::vector<int> p_rowseq_h;
   void start_cache(int rows, int cap, const int32_t* row_seq) override {
     if (p_nseq == 0) throw HrtError(HRT_ERR_INFERENCE, "encode() must precede start_cache()");
-    if (rows < 1 || rows > R_max) throw HrtError(HRT_ERR_INVALID, "rows out of range");
+    if (rows < 1) throw HrtError(HRT_ERR_INVALID, "rows out of range");
+    if (rows > R_max) throw HrtError(HRT_ERR_MEMORY, "rows exceed the arena's max_sentences * max_beam");
     if (cap < 1 || cap > cap_max) throw HrtError(HRT_ERR_INVALID, "cache capacity out of range");
     p_rows = rows;
     p_cap = cap;
+    note_high_water(1, ArenaDims{0, rows, 0, 0});
     p_len = 0;
     p_last_pos = -1;
     p_has_cache = true;
@@ -1604,6 +1490,7 @@ struct Engine : EngineBase {
     int max_src = *std::max_element(p_seq_len.begin(), p_seq_len.end());
     decoder_parallel(M2, B, Tn, max_src, d_off, d_slot, d_qlen, d_map, p_doff, p_dlen, d_keyok, mode, nullptr, d_items,
                      (int)items.size() / 2);
+    note_high_water(2, ArenaDims{0, 0, M2, 0});
     if (p_logits_cap < (size_t)M2 * V) {
       cudaFree(p_logits);
       CUDA_OK(cudaMalloc(&p_logits, (size_t)M2 * V * sizeof(float)));
@@ -1704,81 +1591,6 @@ struct Engine : EngineBase {
     }
   }
 
-  // prefetch slot depth (32-wide K chunks per warp) that fits the shared-memory budget
-  int mega_npf() const {
-    int npf = 8;
-    while (npf > 0 && mega_smem_bytes(d, ff, npf) > 227 * 1024) --npf;
-    return npf;
-  }
-  bool mega_ok() const {
-    return BF16 && use_mega && dh == 64 && d % 128 == 0 && d <= 1024 && ff % 32 == 0 && Ld <= MG_MAX_LAYERS &&
-           timed_class == 0 && s1_skip == 0 && cap_max <= MG_THREADS && mega_npf() >= 1;
-  }
-  // Stage-I steps [t0, t1) in the cooperative tail megakernel (rows <= MG_RMAX)
-  void launch_mega(int t0, int t1, int k, int nrows, const GreedyState& gs) {
-    MegaParams mp{};
-    mp.d = d;
-    mp.ff = ff;
-    mp.H = H;
-    mp.V = V;
-    mp.Ld = Ld;
-    mp.cap = cap_max;
-    mp.k = k;
-    mp.rcap = R_max;
-    for (int i = 0; i < Ld; ++i) {
-      const DecW& w = dec[i];
-      mp.L[i] = MegaLayer{reinterpret_cast<const bf16*>(w.wqkv), reinterpret_cast<const bf16*>(w.wo),
-                          reinterpret_cast<const bf16*>(w.wqc),  reinterpret_cast<const bf16*>(w.woc),
-                          reinterpret_cast<const bf16*>(w.w1),   reinterpret_cast<const bf16*>(w.w2),
-                          w.bqkv, w.bo, w.bqc, w.boc, w.b1, w.b2, w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.ln3g, w.ln3b};
-    }
-    mp.lng = dec_lng;
-    mp.lnb = dec_lnb;
-    mp.E = reinterpret_cast<const bf16*>(E);
-    mp.pe = pe;
-    mp.scale = emb_scale;
-    mp.att_scale = att_scale;
-    mp.xkv = reinterpret_cast<const bf16*>(xkv);
-    mp.xstride = Ld * 2 * d;
-    mp.src_off = s_srcoff;
-    mp.src_len = s_srclen;
-    mp.kc = reinterpret_cast<bf16*>(s1.kc);
-    mp.vc = reinterpret_cast<bf16*>(s1.vc);
-    mp.x = s1.x;
-    mp.q = mg_q;
-    mp.ctx = mg_ctx;
-    mp.hid = mg_hid;
-    mp.vpart = mg_vpart;
-    mp.veos = mg_veos;
-    mp.st = gs;
-    mp.ctl = s_ctl;
-    mp.alive = s_alive;
-    mp.bar = mg_bar;
-    mp.t_begin = t0;
-    mp.t_end = t1;
-    mp.nrows = nrows;
-    mp.trace = mg_trace_on ? mg_trace : nullptr;
-    mp.trace_step = t0 + mg_trace_step;
-    mp.skip = mg_skip;
-    mp.npf = mega_npf();
-    const size_t smem = mega_smem_bytes(d, ff, mp.npf);
-    CUDA_OK(cudaMemsetAsync(mg_bar, 0, sizeof(unsigned), stream));
-    smem_optin(decode_mega_kernel, 227 * 1024);
-    if (smem > 227 * 1024) throw HrtError(HRT_ERR_INVALID, "megakernel shared memory too large");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(num_sms);
-    cfg.blockDim = dim3(MG_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr2[1];
-    attr2[0].id = cudaLaunchAttributeCooperative;
-    attr2[0].val.cooperative = 1;
-    cfg.attrs = attr2;
-    cfg.numAttrs = 1;
-    Scope sc(this, K_OTHER, 0, 0);
-    CUDA_OK(cudaLaunchKernelEx(&cfg, decode_mega_kernel, mp));
-  }
-
   // Capture (once per row bucket and beam width) the Stage-I step as the body
   // of a conditional WHILE node. Every step-varying value lives in s_ctl.
   // U consecutive Stage-I steps captured as one plain graph (no conditional
@@ -1842,12 +1654,6 @@ struct Engine : EngineBase {
 
   void argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, float* lp) override;
 
-  void debug_trace(int64_t* out, int n) override {
-    if (!mg_trace) throw HrtError(HRT_ERR_INVALID, "enable option mega_trace first");
-    CUDA_OK(cudaStreamSynchronize(stream));
-    CUDA_OK(cudaMemcpy(out, mg_trace, std::min(n, 64) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  }
-
   void drop_loop_graphs() {  // options that change kernel choice invalidate the captured loops
     for (auto* m : {&loop_graphs, &plain_graphs}) {
       for (auto& kv : *m) {
@@ -1887,8 +1693,6 @@ struct Engine : EngineBase {
       cluster_min_mtiles = value;
       drop_loop_graphs();
     }
-    else if (name == "mega")
-      use_mega = value != 0;
     else if (name == "attn_heads")
       attn_heads_mode = value;
     else if (name == "attn_rows") {
@@ -1904,19 +1708,9 @@ struct Engine : EngineBase {
       }
       drop_loop_graphs();
     }
-    else if (name == "mega_trace_step")
-      mg_trace_step = value;
     else if (name == "s1_skip") {  // debug: skip Stage-I kernel classes (timing attribution only; wrong results)
       s1_skip = value;
       drop_loop_graphs();
-    } else if (name == "mega_skip")
-      mg_skip = value;
-    else if (name == "mega_trace") {
-      mg_trace_on = value != 0;
-      if (mg_trace_on && !mg_trace) {
-        CUDA_OK(cudaMalloc(&mg_trace, 64 * sizeof(unsigned long long)));
-        CUDA_OK(cudaMemset(mg_trace, 0, 64 * sizeof(unsigned long long)));
-      }
     }
     else if (name == "stage1_skip") {
       s1_skip = value;
@@ -1927,7 +1721,7 @@ struct Engine : EngineBase {
   }
 
   void translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
-                 const int32_t* caps, const hrt_translate_out* out, int on_device) override;
+                 const int32_t* caps, const hrt_translate_out* out, int on_device, bool at) override;
 };
 
 // ---------------------------------------------------------------------------
@@ -2058,9 +1852,16 @@ void Engine<T>::argmax_logprobs(const int32_t* excl, int n_excl, int32_t* amax, 
 // ---------------------------------------------------------------------------
 template <typename T>
 void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k, int b_at, int b_nat, float alpha,
-                          const int32_t* caps, const hrt_translate_out* out, int on_device) {
-  if (B < 1 || B > Bmax) throw HrtError(HRT_ERR_INVALID, "batch size out of range");
-  if (k < 2 || k > cfg.max_chunk) throw HrtError(HRT_ERR_DECODING, "chunk size k not supported by the engine");
+                          const int32_t* caps, const hrt_translate_out* out, int on_device, bool at) {
+  if (B < 1) throw HrtError(HRT_ERR_INVALID, "batch size out of range");
+  if (B > Bmax)  // a phase plan larger than the arena (arena.py:38-42)
+    throw HrtError(HRT_ERR_MEMORY, "batch of " + std::to_string(B) + " sentences exceeds the arena's max_sentences " +
+                                       std::to_string(Bmax));
+  // at: the autoregressive baseline (decoding.py:163-185) on the same captured
+  // Stage-I loop -- interval 1 from BOS, no Stage II (greedy only on this face)
+  if (at && (k != 1 || b_at != 1 || b_nat != 1))
+    throw HrtError(HRT_ERR_INVALID, "the fused AT path is greedy (beam 1); use the session protocol for AT beam search");
+  if (!at && (k < 2 || k > cfg.max_chunk)) throw HrtError(HRT_ERR_DECODING, "chunk size k not supported by the engine");
   if (b_nat < 1 || b_at < b_nat) throw HrtError(HRT_ERR_DECODING, "need b_at >= b_nat >= 1");
   if (b_at > beam_max) throw HrtError(HRT_ERR_INVALID, "b_at exceeds engine max_beam");
   if (b_at > BEAM_MAX) throw HrtError(HRT_ERR_INVALID, "b_at > 7 unsupported by the device beam search");
@@ -2072,12 +1873,29 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     if (lens[i] < 1) throw HrtError(HRT_ERR_INVALID, "empty source");
     raw_off[i + 1] = raw_off[i] + lens[i];
     S[i] = std::min<int>(lens[i], Lmax);
-    cap[i] = caps ? caps[i] : cdiv(Lmax, k);
+    cap[i] = caps ? caps[i] : (at ? Lmax : cdiv(Lmax, k));  // decoding.py:174 / :202-203
     if (cap[i] < 1) throw HrtError(HRT_ERR_INVALID, "max_steps must be >= 1");
     if (cap[i] + 1 > cap_max || k * cap[i] + 1 > P)
       throw HrtError(HRT_ERR_INVALID, "max_steps exceeds the positional table / cache capacity");
   }
-  if (raw_off[B] > Me_max + Bmax) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed capacity");
+  // host ids: validated here (the reference's np.take raises IndexError) and
+  // packed already truncated to max_len, so the capacity check sees the
+  // truncated total; device ids keep their raw offsets (the gather kernel
+  // truncates, and clamps out-of-range ids to EOS instead of reading past E)
+  const bool host_io = on_device != 1;
+  std::vector<int> trunc_off;
+  if (host_io) {
+    trunc_off.assign(B + 1, 0);
+    for (int i = 0; i < B; ++i) {
+      trunc_off[i + 1] = trunc_off[i] + S[i];
+      const int32_t* src = ids + raw_off[i];
+      for (int j = 0; j < lens[i]; ++j)
+        if (src[j] < 0 || src[j] >= V)
+          throw HrtError(HRT_ERR_INVALID, "source token id " + std::to_string(src[j]) + " out of range [0, " +
+                                              std::to_string(V) + ")");
+    }
+    if (trunc_off[B] > Me_max) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed max_src_tokens");
+  }
   std::vector<int> perm(B);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cap[a] > cap[b]; });
@@ -2102,6 +1920,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   if (Mtok > Me_max) throw HrtError(HRT_ERR_MEMORY, "source tokens exceed max_src_tokens");
   const int M2 = off2[C], Mm = moff[C];
   if (M2 > M2_max) throw HrtError(HRT_ERR_MEMORY, "stage-II rows exceed capacity");
+  for (int ph = 0; ph < (at ? 2 : 3); ++ph) note_high_water(ph, ArenaDims{Mtok, B * beam, M2, Mm});
   // Stage-I rows alive at step t: beam rows of every sentence whose cap > t
   // (a prefix of the cap-sorted batch)
   std::vector<int> alive(max_cap, 0);
@@ -2119,7 +1938,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   for (int s = 0; s <= B; ++s) cand_beg[s] = s * bn;
   meta_reset();
   size_t cur = meta_hdr;
-  int* d_rawoff = meta_put(cur, raw_off);
+  int* d_rawoff = meta_put(cur, host_io ? trunc_off : raw_off);
   int* d_perm = meta_put(cur, perm);
   int* d_off = meta_put(cur, off);
   int* d_len = meta_put(cur, len);
@@ -2134,13 +1953,13 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   const std::vector<int> enc_items = prefill_items(len), s2_items = prefill_items(slot);
   int* d_enc_items = meta_put(cur, enc_items);
   int* d_s2_items = meta_put(cur, s2_items);
-  // host source ids ride in the same pinned metadata copy (one H2D transfer per call)
-  const bool host_io = on_device != 1;
+  // host source ids (truncated) ride in the same pinned metadata copy (one H2D transfer per call)
   int* d_ids_meta = nullptr;
-  if (host_io && cur + raw_off[B] <= (size_t)meta_cap) {
-    std::memcpy(h_meta + cur, ids, (size_t)raw_off[B] * sizeof(int));
+  const bool ids_in_meta = host_io && cur + trunc_off[B] <= (size_t)meta_cap;
+  if (ids_in_meta) {
+    for (int i = 0; i < B; ++i) std::memcpy(h_meta + cur + trunc_off[i], ids + raw_off[i], (size_t)S[i] * sizeof(int));
     d_ids_meta = d_meta + cur;
-    cur = (cur + raw_off[B] + 7) & ~size_t(7);
+    cur = (cur + trunc_off[B] + 7) & ~size_t(7);
   }
   {  // fixed header: loop control + alive[] + source offsets/lengths
     StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, B, 0, 0};
@@ -2149,20 +1968,24 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     for (int t = 0; t <= cap_max; ++t) ha[t] = t < max_cap ? alive[t] : 0;
     int* ho = ha + align_up(cap_max + 1, 8);
     std::copy(off.begin(), off.end(), ho);
-    int* hl = ho + align_up(Bmax + 1, 8);
+    std::fill(ho + B + 1, ho + R_max + 1, off[B]);
+    int* hl = ho + align_up(R_max + 1, 8);
     std::copy(len.begin(), len.end(), hl);
+    std::fill(hl + B, hl + R_max, 0);
   }
   meta_flush(cur);
   const int* src_ids = ids;
   if (d_ids_meta) {
     src_ids = d_ids_meta;
-  } else if (host_io) {
-    CUDA_OK(cudaMemcpyAsync(d_ids_raw, ids, raw_off[B] * sizeof(int), cudaMemcpyHostToDevice, stream));
+  } else if (host_io) {  // (unreachable with the metadata sizing; kept for a smaller meta_cap)
+    for (int i = 0; i < B; ++i)
+      CUDA_OK(cudaMemcpyAsync(d_ids_raw + trunc_off[i], ids + raw_off[i], (size_t)S[i] * sizeof(int),
+                              cudaMemcpyHostToDevice, stream));
     src_ids = d_ids_raw;
   }
   {
     Scope sc(this, K_OTHER, 8.0 * Mtok, 0);
-    launch(gather_sentences_kernel, B, 128, 0, src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B);
+    launch(gather_sentences_kernel, B, 128, 0, src_ids, d_rawoff, d_off, d_perm, d_ids, d_pos, B, V);
     check_launch();
   }
   if (debug_spin_us > 0) debug_spin_kernel<<<1, 32, 0, stream>>>((long long)debug_spin_us * 1000);
@@ -2174,7 +1997,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   // cache capacity max_steps + 1 (start_cache, decoding.py:97); the fused path
   // keeps the engine-wide stride cap_max so captured graphs stay valid
   const int capA = cap_max;
-  const int bos = 4 + (k - 2);  // BOS_k (data.py:16)
+  const int bos = at ? BOS_ID : 4 + (k - 2);  // BOS / BOS_k (data.py:14-16)
   CUDA_OK(cudaMemcpyAsync(s_caps, d_caps, B * sizeof(int), cudaMemcpyDeviceToDevice, stream));
   GreedyState gs{E, pe, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, emb_scale, d,
                  s_feed, s_done, s_nsteps, s_forced, s_score, s_anchors, s_caps, capA};
@@ -2188,19 +2011,13 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
       launch(beam_init_kernel, cdiv(B * beam, 128), 128, 0, bs, B, bos);
     check_launch();
     if (!greedy_mode) {
-      launch(rowseq_fill_kernel, cdiv(B * beam, 128), 128, 0, s_rowseq, B * beam, beam);
+      launch(rowseq_fill_kernel, cdiv(R_max, 128), 128, 0, s_rowseq, B * beam, R_max, beam, B);
       check_launch();
     }
   }
   {  // step-0 input (BOS_k at position 0); later steps are embedded by the selection kernel
     Tag _tg(this, "s1.embed_ln");
     embed_ln(s_feed, nullptr, 0, alive.empty() ? 0 : alive[0], dec[0].ln1g, dec[0].ln1b, s1.x, s1.y);
-  }
-  // steps whose live rows fit the tail megakernel run there (greedy, bf16)
-  int t_mega = max_cap;
-  if (greedy_mode && mega_ok()) {
-    t_mega = 0;
-    while (t_mega < max_cap && alive[t_mega] > MG_RMAX) ++t_mega;
   }
   // Stage-I steps in segments of constant row bucket (power of two >= live
   // rows): each segment is one launch of its bucket's captured loop graph, so
@@ -2216,16 +2033,21 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     explicit PrefetchScope(bool& flag) : f(flag) { f = true; }
     ~PrefetchScope() { f = false; }
   } pscope(cross_prefetch);
-  for (int t0 = 0; t0 < t_mega && alive[t0] > 0;) {
+  for (int t0 = 0; t0 < max_cap && alive[t0] > 0;) {
     const int bucket = bucket_of(alive[t0]);
     int t1 = t0;
-    while (t1 < t_mega && alive[t1] > 0 && bucket_of(alive[t1]) == bucket) ++t1;
-    {  // loop control for this segment (the finished count carries over); the copy also
-       // orders every earlier kernel (encoder) before Stage I (cross_prefetch relies on it)
-      const int hdr[5] = {t0, alive[t0], t0 * k, k, t1};
+    while (t1 < max_cap && alive[t1] > 0 && bucket_of(alive[t1]) == bucket) ++t1;
+    const bool unrolled = BF16 && use_graphs && timed_class == 0 && graph_unroll > 0;
+    if (!unrolled || t0 == 0) {
+      // loop control (the finished count carries over); the copy also orders every
+      // earlier kernel (encoder) before Stage I (cross_prefetch relies on it). The
+      // unrolled graphs need it once: their advance kernel steps t / R / pos across
+      // segment boundaries, and sets R = 0 once every row has finished (natural EOS,
+      // decoding.py:149-150), so the remaining captured steps exit at once.
+      const int hdr[5] = {t0, alive[t0], t0 * k, k, unrolled ? max_cap : t1};
       CUDA_OK(cudaMemcpyAsync(s_ctl, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream));
     }
-    if (BF16 && use_graphs && timed_class == 0 && graph_unroll > 0) {
+    if (unrolled) {
       // n steps as U-step graphs, U = graph_unroll, graph_unroll / 2, ..., 1
       // (binary decomposition: at most log2(graph_unroll) + 1 graphs per bucket)
       int left = t1 - t0;
@@ -2256,11 +2078,12 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     }
     t0 = t1;
   }
-  if (t_mega < max_cap) launch_mega(t_mega, max_cap, k, B, gs);
   phase_mark(2);
   // ---- phase 3: Stage II over the selected candidates ----
   Stage2Cands cands;
-  if (greedy_mode) {
+  if (at) {
+    cands = Stage2Cands{s_anchors, nullptr, capA, s_nsteps, s_score, s_forced, s_nsteps};
+  } else if (greedy_mode) {
     cands = Stage2Cands{s_anchors, nullptr, capA, s_nsteps, s_score, s_forced, s_nsteps};
   } else {
     Scope sc(this, K_OTHER, 0, 0);
@@ -2268,19 +2091,21 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     check_launch();
     cands = Stage2Cands{b_ftok, c_off, capA, c_len, c_sat, c_forced, bs.nsteps};
   }
-  {
-    Scope sc(this, K_OTHER, 0, 0);
-    launch(stage2_build_kernel, C, 128, 0, cands, d_off2, d_slot, C, k, s2.ids, s2.pos, d_qlen2);
-    check_launch();
-  }
-  decoder_parallel(M2, C, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
-                   d_s2_items, (int)s2_items.size() / 2);
-  Tag _tg2(this, "stage2.vocab");
-  vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
-  {
-    Scope sc(this, K_OTHER, 0, 0);
-    launch(rowstat_kernel<1>, cdiv(Mm, 4), 128, 0, s2.parts, Mm, 1, s2.mstat, (const int*)nullptr);
-    check_launch();
+  if (!at) {
+    {
+      Scope sc(this, K_OTHER, 0, 0);
+      launch(stage2_build_kernel, C, 128, 0, cands, d_off2, d_slot, C, k, s2.ids, s2.pos, d_qlen2);
+      check_launch();
+    }
+    decoder_parallel(M2, C, max_slot, max_src, d_off2, d_slot, d_qlen2, d_seqmap, d_off, d_len, nullptr, 0, d_outrow,
+                     d_s2_items, (int)s2_items.size() / 2);
+    Tag _tg2(this, "stage2.vocab");
+    vocab_parts(s2.ymask, Mm_max, Mm, s2.parts, 1, 1, s2.logits);
+    {
+      Scope sc(this, K_OTHER, 0, 0);
+      launch(rowstat_kernel<1>, cdiv(Mm, 4), 128, 0, s2.parts, Mm, 1, s2.mstat, (const int*)nullptr);
+      check_launch();
+    }
   }
   Stage2Out so;
   so.tokens = host_io ? o_tokens : out->tokens;
@@ -2305,8 +2130,11 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   so.out_index = d_perm;
   {
     Scope sc(this, K_OTHER, 0, 0);
-    launch(stage2_finish_kernel, cdiv(B, 4), 128, 0, s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, cands, k,
-           alpha, Lmax, B, so);
+    if (at)
+      launch(at_finish_kernel, cdiv(B, 4), 128, 0, cands, alpha, Lmax, B, so);
+    else
+      launch(stage2_finish_kernel, cdiv(B, 4), 128, 0, s2.ids, d_off2, d_qlen2, d_moff, s2.mstat, d_cbeg, cands, k,
+             alpha, Lmax, B, so);
     check_launch();
   }
   phase_mark(3);
@@ -2334,189 +2162,3 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
 }
 
 }  // namespace hrt
-
-// ===========================================================================
-// C ABI
-// ===========================================================================
-using namespace hrt;
-
-struct hrt_engine {
-  std::unique_ptr<EngineBase> impl;
-};
-
-static std::string g_last_error;
-
-template <class Fn>
-static hrt_status guarded(hrt_engine* eng, Fn&& fn) {
-  try {
-    if (eng) cudaSetDevice(eng->impl->device);
-    fn();
-    return HRT_OK;
-  } catch (const HrtError& e) {
-    if (eng) eng->impl->last_error = e.what();
-    g_last_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    if (eng) eng->impl->last_error = e.what();
-    g_last_error = e.what();
-    return HRT_ERR_CUDA;
-  }
-}
-
-extern "C" {
-
-int64_t hrt_param_count(const hrt_config* cfg) { return Engine<float>::param_count(*cfg); }
-
-hrt_status hrt_create(const hrt_config* cfg, const float* params, int64_t n_params, int32_t device, hrt_engine** out) {
-  return guarded(nullptr, [&] {
-    if (!cfg || !params || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
-    if (n_params != Engine<float>::param_count(*cfg))
-      throw HrtError(HRT_ERR_INVALID, "n_params " + std::to_string(n_params) + " != expected " +
-                                          std::to_string(Engine<float>::param_count(*cfg)));
-    auto e = std::make_unique<hrt_engine>();
-    if (cfg->dtype == HRT_DTYPE_F32)
-      e->impl.reset(new Engine<float>(*cfg, params, device));
-    else if (cfg->dtype == HRT_DTYPE_BF16)
-      e->impl.reset(new Engine<bf16>(*cfg, params, device));
-    else
-      throw HrtError(HRT_ERR_INVALID, "unknown dtype");
-    *out = e.release();
-  });
-}
-
-void hrt_destroy(hrt_engine* eng) { delete eng; }
-
-const char* hrt_last_error(const hrt_engine* eng) {
-  return eng ? eng->impl->last_error.c_str() : g_last_error.c_str();
-}
-
-hrt_status hrt_get_stats(const hrt_engine* eng, hrt_stats* out) {
-  if (!eng || !out) return HRT_ERR_INVALID;
-  *out = eng->impl->stats;
-  return HRT_OK;
-}
-
-void* hrt_stream(hrt_engine* eng) { return eng ? (void*)eng->impl->stream : nullptr; }
-
-hrt_status hrt_synchronize(hrt_engine* eng) {
-  return guarded(eng, [&] { CUDA_OK(cudaStreamSynchronize(eng->impl->stream)); });
-}
-
-hrt_status hrt_encode(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t n_seq, float* memory_out) {
-  return guarded(eng, [&] { eng->impl->encode(ids, lens, n_seq, memory_out); });
-}
-
-hrt_status hrt_start_cache(hrt_engine* eng, int32_t rows, int32_t cap, const int32_t* row_seq) {
-  return guarded(eng, [&] { eng->impl->start_cache(rows, cap, row_seq); });
-}
-
-hrt_status hrt_step(hrt_engine* eng, const int32_t* tokens, int32_t position, float* logp_out) {
-  return guarded(eng, [&] { eng->impl->step(tokens, position, logp_out); });
-}
-
-hrt_status hrt_reorder(hrt_engine* eng, const int32_t* parents) {
-  return guarded(eng, [&] { eng->impl->reorder(parents); });
-}
-
-hrt_status hrt_parallel_logits(hrt_engine* eng, const int32_t* ids, const int32_t* positions, const uint8_t* pad_mask,
-                               int32_t B, int32_t T, int32_t mode, const int32_t* seq, float* logits_out) {
-  return guarded(eng, [&] { eng->impl->parallel_logits(ids, positions, pad_mask, B, T, mode, seq, logits_out); });
-}
-
-hrt_status hrt_argmax_logprobs(hrt_engine* eng, const int32_t* exclude, int32_t n_exclude, int32_t* amax_out,
-                               float* lp_out) {
-  return guarded(eng, [&] { eng->impl->argmax_logprobs(exclude, n_exclude, amax_out, lp_out); });
-}
-
-hrt_status hrt_translate_batch(hrt_engine* eng, const int32_t* ids, const int32_t* lens, int32_t B, int32_t k,
-                               int32_t b_at, int32_t b_nat, float length_penalty, const int32_t* max_steps,
-                               const hrt_translate_out* out, int32_t io_on_device) {
-  return guarded(eng, [&] {
-    if (!ids || !lens || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
-    eng->impl->translate(ids, lens, B, k, b_at, b_nat, length_penalty, max_steps, out, io_on_device);
-  });
-}
-
-hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value) {
-  return guarded(eng, [&] { eng->impl->set_option(name ? name : "", value); });
-}
-
-hrt_status hrt_phase_times(hrt_engine* eng, float* ms3) {
-  return guarded(eng, [&] {
-    EngineBase* e = eng->impl.get();
-    if (!e->phase_valid) throw HrtError(HRT_ERR_INVALID, "no fused call recorded yet");
-    CUDA_OK(cudaEventSynchronize(e->phase_ev[3]));
-    for (int i = 0; i < 3; ++i) CUDA_OK(cudaEventElapsedTime(&ms3[i], e->phase_ev[i], e->phase_ev[i + 1]));
-  });
-}
-
-hrt_status hrt_debug_trace(hrt_engine* eng, int64_t* out, int32_t n) {
-  return guarded(eng, [&] { eng->impl->debug_trace(out, n); });
-}
-
-hrt_status hrt_timing_enable(hrt_engine* eng, const char* kernel_class, int32_t enable) {
-  return guarded(eng, [&] {
-    EngineBase* e = eng->impl.get();
-    int cls = 0;
-    std::string c = kernel_class ? kernel_class : "all";
-    if (c == "vocab") cls = K_VOCAB;
-    else if (c == "gemm") cls = K_GEMM;
-    else if (c == "attn") cls = K_ATTN;
-    else if (c == "all") cls = K_GEMM | K_VOCAB | K_ATTN | K_OTHER;
-    else throw HrtError(HRT_ERR_INVALID, "unknown kernel class " + c);
-    CUDA_OK(cudaStreamSynchronize(e->stream));
-    e->timed_class = enable ? cls : 0;
-    e->ev_used = 0;
-    e->t_bytes = e->t_flops = 0;
-    e->t_launches = 0;
-  });
-}
-
-hrt_status hrt_timing_report(hrt_engine* eng, char* buf, int64_t cap) {
-  return guarded(eng, [&] {
-    EngineBase* e = eng->impl.get();
-    CUDA_OK(cudaStreamSynchronize(e->stream));
-    struct Agg {
-      double ms = 0, flops = 0;
-      int n = 0;
-    };
-    std::map<std::string, Agg> agg;
-    for (size_t i = 0; i < e->ev_used; ++i) {
-      float m = 0;
-      CUDA_OK(cudaEventElapsedTime(&m, e->ev_pool[i].first, e->ev_pool[i].second));
-      Agg& a = agg[e->ev_tag[i] ? e->ev_tag[i] : "untagged"];
-      a.ms += m;
-      a.n += 1;
-      a.flops += e->ev_flops[i];
-    }
-    std::string s = "{";
-    for (auto& kv : agg) {
-      if (s.size() > 1) s += ", ";
-      s += "\"" + kv.first + "\": [" + std::to_string(kv.second.ms) + ", " + std::to_string(kv.second.n) + ", " +
-           std::to_string(kv.second.flops) + "]";
-    }
-    s += "}";
-    if ((int64_t)s.size() + 1 > cap) throw HrtError(HRT_ERR_INVALID, "report buffer too small");
-    std::memcpy(buf, s.c_str(), s.size() + 1);
-  });
-}
-
-hrt_status hrt_timing_read(hrt_engine* eng, double* total_ms, int64_t* launches, double* alg_bytes,
-                           double* alg_flops) {
-  return guarded(eng, [&] {
-    EngineBase* e = eng->impl.get();
-    CUDA_OK(cudaStreamSynchronize(e->stream));
-    double ms = 0;
-    for (size_t i = 0; i < e->ev_used; ++i) {
-      float m = 0;
-      CUDA_OK(cudaEventElapsedTime(&m, e->ev_pool[i].first, e->ev_pool[i].second));
-      ms += m;
-    }
-    if (total_ms) *total_ms = ms;
-    if (launches) *launches = e->t_launches;
-    if (alg_bytes) *alg_bytes = e->t_bytes;
-    if (alg_flops) *alg_flops = e->t_flops;
-  });
-}
-
-}  // extern "C"

@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
                                : make_uint4(0, 0, 0, 0);
   }
   if (M_dev) M = *M_dev;
+  if (M <= 0) return;  // every Stage-I row finished (uniform across the CTA)
   // The final reduction and epilogue are spread over NG warps: warp w < NG owns
   // n-tiles w, w + NG, ...; its epilogue operands (residual rows, bias) are
   // issued now and consumed after the reduction.
@@ -414,6 +415,7 @@ __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* 
     for (int i = 0; i < GV_MAXC; ++i) a0[i] = *reinterpret_cast<const uint4*>(ar + 32 * min(i, nch - 1));
   }
   if (M_dev) M = *M_dev;
+  if (M <= 0) return;  // every Stage-I row finished (uniform across the CTA)
   if (LNA) {
     gv_ln_stats(ln, M, K, lnst);
     __syncthreads();

@@ -1629,10 +1629,14 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
 
 // Same step advance for the unrolled (plain) loop graphs: the host launches
 // exactly the segment's step count, so no loop condition is set.
+// Once every row (sentence, in beam mode) has finished, R drops to 0 and the
+// remaining captured steps' kernels return immediately.
 __global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive) {
   pdl_enter();
   const int t = ctl->t + 1;
-  if (t < ctl->max_cap && alive[t] > 0) {
+  if (ctl->finished >= ctl->nrows) {
+    ctl->R = 0;
+  } else if (t < ctl->max_cap && alive[t] > 0) {
     ctl->t = t;
     ctl->R = alive[t];
     ctl->pos = t * ctl->k;
@@ -1704,6 +1708,39 @@ struct Stage2Out {
   unsigned char* forced;  // [S]
   const int* out_index;   // [S] -> output slot (undo the length sort)
 };
+
+// AT baseline result (decoding.py:173-185, beam 1): the finished hypothesis'
+// tokens up to its EOS, score s / len^alpha with len counting the EOS,
+// decoder_calls = Stage-I steps. One warp per sentence.
+__global__ void at_finish_kernel(Stage2Cands cands, float alpha, int max_len, int S, Stage2Out out) {
+  pdl_enter();
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  const int m = cands.len[s];  // generated tokens including EOS (= steps for greedy)
+  const int* tok = cands.tok + (size_t)s * cands.cap;
+  int first_eos = m;
+  for (int j0 = 0; j0 < m; j0 += 32) {
+    const int j = j0 + lane;
+    const unsigned ball = __ballot_sync(0xffffffffu, j < m && tok[j] == EOS_ID);
+    if (ball) {
+      first_eos = j0 + __ffs(ball) - 1;
+      break;
+    }
+  }
+  const int n = min(first_eos, max_len);
+  const int dst = out.out_index ? out.out_index[s] : s;
+  for (int j = lane; j < n; j += 32) out.tokens[(size_t)dst * max_len + j] = tok[j];
+  if (lane == 0) {
+    const double sat = cands.s_at[s];
+    out.lens[dst] = n;
+    out.scores[(size_t)dst * 3 + 0] = sat;
+    out.scores[(size_t)dst * 3 + 1] = 0.0;
+    out.scores[(size_t)dst * 3 + 2] = sat / pow((double)max(m, 1), (double)alpha);
+    out.calls[dst] = cands.steps[s];
+    out.forced[dst] = (unsigned char)cands.forced[s];
+  }
+}
 
 __global__ void stage2_finish_kernel(const int* __restrict__ ids, const int* __restrict__ off,
                                      const int* __restrict__ qlen, const int* __restrict__ mrow_off,
@@ -2090,7 +2127,7 @@ __global__ void beam_candidates_kernel(BeamState st, int S, int* __restrict__ c_
 // packed gather of sentences into a new order: dst sentence i <- src sentence perm[i]
 __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* __restrict__ src_off,
                                         const int* __restrict__ dst_off, const int* __restrict__ perm,
-                                        int* __restrict__ dst, int* __restrict__ pos, int n) {
+                                        int* __restrict__ dst, int* __restrict__ pos, int n, int vocab) {
   pdl_enter();
   const int i = blockIdx.x;
   if (i >= n) return;
@@ -2099,7 +2136,8 @@ __global__ void gather_sentences_kernel(const int* __restrict__ src, const int* 
   // tokens (decoding.py:260 truncation); the raw offsets still step over the full source
   const int so = src_off[p], d0 = dst_off[i], len = min(src_off[p + 1] - so, dst_off[i + 1] - d0);
   for (int j = threadIdx.x; j < len; j += blockDim.x) {
-    dst[d0 + j] = src[so + j];
+    const int id = src[so + j];
+    dst[d0 + j] = (id >= 0 && id < vocab) ? id : EOS_ID;  // device ids are not validated on the host
     pos[d0 + j] = j;
   }
 }
@@ -2128,10 +2166,13 @@ __global__ void stage1_init_kernel(int R, int cap, int bos, int* feed, int* done
 }
 
 // Stage-I row -> encoded sentence (beam rows share their sentence's memory)
-__global__ void rowseq_fill_kernel(int* __restrict__ rowseq, int rows, int beam) {
+// Rows past the live ones (up to the graph's row bucket) name sentence B,
+// whose source length in the header is 0: the cross-attention K/V prefetch,
+// which runs before the row count resolves, then reads nothing.
+__global__ void rowseq_fill_kernel(int* __restrict__ rowseq, int rows, int rows_cap, int beam, int n_seq) {
   pdl_enter();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < rows) rowseq[r] = r / beam;
+  if (r < rows_cap) rowseq[r] = r < rows ? r / beam : n_seq;
 }
 
 // Beam reorder as an index permutation (infer.py:307-318): row j continues

@@ -182,6 +182,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
       }
+      // no unit after all (device row count 0: every Stage-I row finished): the stages
+      // armed before the PDL wait expect their A tiles too -- load them (rows past the
+      // tensor are zero-filled by TMA) so every byte lands before the CTA may exit
+      if (cid >= num_units) {
+        const int kb0 = (cid % S) * num_kb / S;
+        for (int s2 = 0; s2 < pre; ++s2)
+          tma_load_2d(smem + s2 * L::STAGE_BYTES, &tmA, &full[s2], (kb0 + s2) * TC_BK, 0);
+        for (int s2 = 0; s2 < pre; ++s2) mbar_wait(&full[s2], 0);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {

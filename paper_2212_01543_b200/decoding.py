@@ -32,7 +32,7 @@ from .model import BOS, BOS_K, EOS, EXCLUDED_OUTPUT_IDS, MASK, PAD
 __all__ = [
     "DecodingError", "EXCLUDED_OUTPUT_IDS", "Hypothesis", "Translation", "truncate_at_eos",
     "build_stage2_input", "combined_score", "skip_at_stage", "skip_cmlm_fill", "hrt_translate",
-    "hrt_translate_batch", "at_translate", "PositionedSequence",
+    "hrt_translate_batch", "at_translate", "at_translate_batch", "PositionedSequence",
 ]
 
 
@@ -233,12 +233,30 @@ def hrt_translate_batch(session, sources, k, b_at=1, b_nat=1, length_penalty=0.6
     return [hrt_translate(session, s, k, b_at, b_nat, length_penalty, max_steps=m) for s, m in zip(sources, caps)]
 
 
+def at_translate_batch(session, sources, length_penalty=0.6, max_len=None):
+    """Batched greedy AT baseline: one fused device call with a CudaSession.
+    `max_len` is one cap for all sentences or a per-sentence list."""
+    caps = None
+    if max_len is not None:
+        caps = list(max_len) if hasattr(max_len, "__len__") else [int(max_len)] * len(sources)
+    if isinstance(session, CudaSession):
+        return session.at_translate_batch(list(map(list, sources)), length_penalty, caps)
+    caps = caps or [None] * len(sources)
+    return [at_translate(session, s, 1, length_penalty, m) for s, m in zip(sources, caps)]
+
+
 def at_translate(session, source, beam=1, length_penalty=0.6, max_len=None, ws=None):
-    """Autoregressive baseline from BOS over the same kernels (decoding.py:163-185)."""
+    """Autoregressive baseline from BOS over the same kernels (decoding.py:163-185).
+    Greedy (beam 1) on a CudaSession runs the fused device path; beam search
+    runs the protocol-level search below."""
     if beam < 1:
         raise DecodingError("beam must be >= 1")
     t0 = time.perf_counter()
     max_len = max_len or session.config.max_len
+    if isinstance(session, CudaSession) and beam == 1:  # fused greedy AT on the captured loop
+        tr = session.at_translate_batch([list(source)], length_penalty, [int(max_len)])[0]
+        tr.wall_time = time.perf_counter() - t0
+        return tr
     session.encode(list(source)[: session.config.max_len])
     done, steps = _search(session, BOS, 1, beam, max_len)
     best = max(done, key=lambda h: h.score / len(h.tokens) ** length_penalty)

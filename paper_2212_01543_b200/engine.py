@@ -63,6 +63,34 @@ def _dtype_code(dtype):
     return _DTYPES[key]
 
 
+def estimate_max_bytes(config, dtype="float32", max_sentences=1, max_beam=4, max_src_tokens=0, max_chunk=None):
+    """Closed-form per-phase activation bytes of an engine and its arena
+    capacity (reference infer.py:78-96 `estimate_max_bytes`): keys "encoder",
+    "skip-at", "skip-cmlm", "max". Computed by the engine library's own plan
+    (the one hrt_create allocates), no GPU needed."""
+    lib = _lib.load()
+    c = ModelConfig.from_any(config)
+    cfg = _lib.HrtConfig(c.d_model, c.d_ff, c.n_heads, c.enc_layers, c.dec_layers, c.vocab_size, c.max_len,
+                         int(max_chunk or max(c.chunk_sizes)), _dtype_code(dtype), int(max_sentences), int(max_beam),
+                         int(max_src_tokens))
+    out = (C.c_int64 * 4)()
+    st = lib.hrt_estimate_arena(C.byref(cfg), out)
+    if st != _lib.HRT_OK:
+        raise _ERRORS.get(st, EngineCudaError)(lib.hrt_last_error(None).decode(errors="replace"))
+    return {"encoder": out[0], "skip-at": out[1], "skip-cmlm": out[2], "max": out[3]}
+
+
+def _pinned(shape, dt):
+    """Page-locked host array (torch's pinned allocator when available)."""
+    try:
+        import torch
+
+        tdt = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8}[dt]
+        return torch.zeros(shape, dtype=tdt, pin_memory=True).numpy()
+    except Exception:  # no torch / no CUDA context: pageable (copies then block the host)
+        return np.zeros(shape, dtype=dt)
+
+
 class Engine:
     """One device engine: weights, arena and KV caches live on `device`."""
 
@@ -129,12 +157,6 @@ class Engine:
         self._check(self.lib.hrt_phase_times(self._h, _ptr(ms, C.c_float)))
         return dict(encoder=float(ms[0]), stage1=float(ms[1]), stage2=float(ms[2]))
 
-    def debug_trace(self):
-        """ns stamps of the tail megakernel's phase barriers (option mega_trace)."""
-        buf = np.zeros(64, np.int64)
-        self._check(self.lib.hrt_debug_trace(self._h, _ptr(buf, C.c_int64), 64))
-        return buf
-
     def timing_enable(self, kernel_class="all", enable=True):
         self._check(self.lib.hrt_timing_enable(self._h, kernel_class.encode(), int(enable)))
 
@@ -166,6 +188,51 @@ class Engine:
                                                  int(b_nat), float(length_penalty), _ptr(ms), C.byref(o), 0))
         return out
 
+    def at_translate_arrays(self, ids, lens, length_penalty=0.6, max_steps=None, out=None, io=0):
+        """Fused greedy AT baseline (decoding.py:163-185) on packed host arrays
+        (io=0), or pinned host arrays without synchronising (io=2)."""
+        lens = _i32(lens)
+        ids = _i32(ids)
+        ms = None if max_steps is None else _i32(max_steps)
+        if out is None:
+            out = self.alloc_outputs(int(lens.size))
+        o = _lib.HrtTranslateOut(out["tokens"].ctypes.data, out["lens"].ctypes.data, out["scores"].ctypes.data,
+                                 out["calls"].ctypes.data, out["forced"].ctypes.data)
+        if io == 2:
+            self._pending = (ids, lens, ms, o)
+        self._check(self.lib.hrt_at_translate_batch(self._h, ids.ctypes.data, _ptr(lens), int(lens.size), 1,
+                                                    float(length_penalty), _ptr(ms), C.byref(o), int(io)))
+        return out
+
+    def at_translate_device(self, ids_dev_ptr, lens, out_ptrs, length_penalty=0.6, max_steps=None):
+        """Fused greedy AT with device-resident ids/outputs (raw CUDA pointers)."""
+        lens = _i32(lens)
+        ms = None if max_steps is None else _i32(max_steps)
+        o = _lib.HrtTranslateOut(*out_ptrs)
+        self._check(self.lib.hrt_at_translate_batch(self._h, C.c_void_p(ids_dev_ptr), _ptr(lens), int(lens.size), 1,
+                                                    float(length_penalty), _ptr(ms), C.byref(o), 1))
+
+    def at_translate_batch(self, sources, length_penalty=0.6, max_steps=None):
+        """List of Translation from the fused greedy AT path."""
+        if not len(sources):
+            return []
+        lens = np.array([len(s) for s in sources], dtype=np.int32)
+        ids = np.concatenate([np.asarray(s, dtype=np.int32) for s in sources])
+        t0 = time.perf_counter()
+        out = self.at_translate_arrays(ids, lens, length_penalty, max_steps)
+        return self._translations(out, len(sources), time.perf_counter() - t0)
+
+    def _translations(self, out, B, wall=0.0):
+        from .decoding import Translation
+
+        res = []
+        for i in range(B):
+            n = int(out["lens"][i])
+            res.append(Translation(tokens=out["tokens"][i, :n].tolist(), skip_at_score=float(out["scores"][i, 0]),
+                                   skip_cmlm_score=float(out["scores"][i, 1]), score=float(out["scores"][i, 2]),
+                                   decoder_calls=int(out["calls"][i]), wall_time=wall, forced=bool(out["forced"][i])))
+        return res
+
     def translate_arrays_async(self, ids, lens, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None, out=None):
         """Like translate_arrays but returns once the work is enqueued; call
         synchronize() before reading `out`. Keep ids/lens/out alive until then
@@ -173,6 +240,8 @@ class Engine:
         lens = _i32(lens)
         ids = _i32(ids)
         ms = None if max_steps is None else _i32(max_steps)
+        if out is None:
+            out = self.alloc_outputs(int(lens.size), pinned=_pinned)
         o = _lib.HrtTranslateOut(out["tokens"].ctypes.data, out["lens"].ctypes.data, out["scores"].ctypes.data,
                                  out["calls"].ctypes.data, out["forced"].ctypes.data)
         self._pending = (ids, lens, ms, o)
@@ -198,8 +267,6 @@ class Engine:
 
     def translate_batch(self, sources, k=2, b_at=1, b_nat=1, length_penalty=0.6, max_steps=None):
         """List of Translation for a list of source id lists (one fused call)."""
-        from .decoding import Translation
-
         if not len(sources):
             return []  # nothing to decode (the C ABI rejects B < 1)
         t0 = time.perf_counter()
@@ -207,14 +274,7 @@ class Engine:
         ids = np.concatenate([np.asarray(s, dtype=np.int32) for s in sources]) if len(sources) else \
             np.zeros(0, np.int32)
         out = self.translate_arrays(ids, lens, k, b_at, b_nat, length_penalty, max_steps)
-        wall = time.perf_counter() - t0
-        res = []
-        for i in range(len(sources)):
-            n = int(out["lens"][i])
-            res.append(Translation(tokens=out["tokens"][i, :n].tolist(), skip_at_score=float(out["scores"][i, 0]),
-                                   skip_cmlm_score=float(out["scores"][i, 1]), score=float(out["scores"][i, 2]),
-                                   decoder_calls=int(out["calls"][i]), wall_time=wall, forced=bool(out["forced"][i])))
-        return res
+        return self._translations(out, len(sources), time.perf_counter() - t0)
 
 
 class DecoderCache:
@@ -335,6 +395,11 @@ class CudaSession:
         self.decoder_calls += sum(t.decoder_calls for t in res)
         return res
 
+    def at_translate_batch(self, sources, length_penalty=0.6, max_steps=None):
+        res = self.engine.at_translate_batch(sources, length_penalty, max_steps)
+        self.decoder_calls += sum(t.decoder_calls for t in res)
+        return res
+
 
 class EnginePool:
     """Concurrent sub-batches on one device: `n` engines, one CUDA stream each.
@@ -351,6 +416,10 @@ class EnginePool:
         self.engines = [Engine(model, dtype=dtype, device=device, max_sentences=per, max_beam=max_beam, **kw)
                         for _ in range(int(n))]
         self.config = self.engines[0].config
+        self.decoder_calls = 0
+        # pinned host outputs per engine: a device-to-host copy into pageable memory
+        # would block the host and serialise the engines
+        self._out = [e.alloc_outputs(per, pinned=_pinned) for e in self.engines]
 
     def split(self, caps):
         """Length buckets: indices sorted by cap (desc), cut into len(engines) runs."""
@@ -367,7 +436,7 @@ class EnginePool:
             srcs = [sources[i] for i in idx]
             lens = np.array([len(s) for s in srcs], np.int32)
             ids = np.concatenate([np.asarray(s, np.int32) for s in srcs])
-            out = eng.alloc_outputs(len(idx))
+            out = {key: arr[: len(idx)] for key, arr in self._out[len(outs)].items()}
             eng.translate_arrays_async(ids, lens, k, b_at, b_nat, length_penalty, [caps[i] for i in idx], out)
             outs.append((idx, out, ids, lens))
         from .decoding import Translation
@@ -380,4 +449,5 @@ class EnginePool:
                 res[i] = Translation(tokens=out["tokens"][j, :n].tolist(), skip_at_score=float(out["scores"][j, 0]),
                                      skip_cmlm_score=float(out["scores"][j, 1]), score=float(out["scores"][j, 2]),
                                      decoder_calls=int(out["calls"][j]), forced=bool(out["forced"][j]))
+            self.decoder_calls += int(out["calls"][: len(idx)].sum())
         return res

@@ -40,14 +40,21 @@ def predicted_cost(src_len, k=2, enc_layers=12):
     return src_len * enc_layers + m * 6 + k * m
 
 
-def length_buckets(lens, max_tokens=8192, k=2, enc_layers=12):
-    """Sort by length (stable) and cut into buckets of <= max_tokens tokens."""
+def length_buckets(lens, max_tokens=8192, k=2, enc_layers=12, padded=True):
+    """Sort by length (stable) and cut into buckets of <= max_tokens tokens.
+
+    padded=True (the BASELINE's C5 batches): a bucket's size is its sentence
+    count times its longest source, as a padded batch would be; the engine
+    itself packs the sentences (no padding reaches a kernel). padded=False
+    counts the real tokens only.
+    """
     lens = np.asarray(lens)
     order = np.argsort(lens, kind="stable")
     buckets, cur, tok, cost = [], [], 0, 0.0
     for i in order:
         li = int(lens[i])
-        if cur and tok + li > max_tokens:
+        grown = (len(cur) + 1) * li if padded else tok + li  # ascending order: li is the bucket maximum
+        if cur and grown > max_tokens:
             buckets.append(Bucket(np.array(cur), tok, cost))
             cur, tok, cost = [], 0, 0.0
         cur.append(int(i))
@@ -69,13 +76,14 @@ def assign_lpt(buckets, world_size):
     return out
 
 
-def shard(lens, rank, world_size, max_tokens=8192, k=2, enc_layers=12):
+def shard(lens, rank, world_size, max_tokens=8192, k=2, enc_layers=12, padded=True):
     """This rank's buckets (deterministic on every rank: no communication)."""
-    return assign_lpt(length_buckets(lens, max_tokens, k, enc_layers), world_size)[rank]
+    return assign_lpt(length_buckets(lens, max_tokens, k, enc_layers, padded), world_size)[rank]
 
 
-def rank_loads(lens, world_size, max_tokens=8192, k=2, enc_layers=12):
-    return [sum(b.cost for b in bs) for bs in assign_lpt(length_buckets(lens, max_tokens, k, enc_layers), world_size)]
+def rank_loads(lens, world_size, max_tokens=8192, k=2, enc_layers=12, padded=True):
+    return [sum(b.cost for b in bs)
+            for bs in assign_lpt(length_buckets(lens, max_tokens, k, enc_layers, padded), world_size)]
 
 
 def gather_outputs(index, lens, tokens, group=None, device=None):

@@ -199,3 +199,42 @@ def test_bench_reference_arm_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_arena_estimate_closed_form(lib_path):
+    """estimate_max_bytes (infer.py:78-96; reference tests/test_infer.py:163-171):
+    every phase reported, max = the largest phase, monotone in the capacity
+    knobs, phases alias (max < sum). Host-only call into the C ABI."""
+    cfg = W.C2
+    est = hrt.estimate_max_bytes(cfg, "bfloat16", max_sentences=64, max_beam=1)
+    assert set(est) == {"encoder", "skip-at", "skip-cmlm", "max"}
+    assert est["max"] == max(v for k, v in est.items() if k != "max")
+    assert est["max"] < est["encoder"] + est["skip-at"] + est["skip-cmlm"]
+    big = hrt.estimate_max_bytes(cfg, "bfloat16", max_sentences=128, max_beam=1)
+    assert all(big[k] >= est[k] for k in est) and big["max"] > est["max"]
+    beam = hrt.estimate_max_bytes(cfg, "bfloat16", max_sentences=64, max_beam=4)
+    assert beam["skip-at"] > est["skip-at"] and beam["encoder"] == est["encoder"]
+    tok = hrt.estimate_max_bytes(cfg, "bfloat16", max_sentences=64, max_beam=1, max_src_tokens=1000)
+    assert tok["encoder"] < est["encoder"]
+    # fp32 activations are wider than bf16 ones
+    assert hrt.estimate_max_bytes(cfg, "float32", max_sentences=64, max_beam=1)["encoder"] > est["encoder"]
+    # encoder phase lower bound: fp32 residual + bf16 y / qkv / ctx / hidden for every token slot
+    me = 64 * cfg.max_len
+    assert est["encoder"] >= me * (4 * 512 + 2 * (512 + 3 * 512 + 512 + 2048))
+
+
+def test_teacher_forced_accounting_flags_real_mismatches():
+    """oracle.greedy_teacher_forced: an oracle decode scores 100 % against
+    itself; flipping one anchor or one fill is counted as a (non-tie) miss."""
+    cfg = O.Config(64, 128, 2, 2, 1, 97, 24)
+    orc = O.Oracle(cfg, O.init_params(cfg, 5), dtype=np.float64)
+    src = [11, 40, 7, 93, 2]
+    cap = O.max_steps_for(len(src) - 1, 2)
+    tr = O.hrt_translate(orc, src, 2, max_steps=cap)
+    r = O.greedy_teacher_forced(orc, src, 2, tr.tokens, cap)
+    assert r["bad"] == 0 and r["s1"] == r["s1_agree"] > 0 and r["s2"] == r["s2_agree"] > 0
+    for j in (0, 1):  # a fill (position 0) and an anchor (position 1)
+        toks = list(tr.tokens)
+        toks[j] = 50 if toks[j] != 50 else 51
+        r = O.greedy_teacher_forced(orc, src, 2, toks, cap)
+        assert r["bad"] + r["s1_ties"] + r["s2_ties"] >= 1

@@ -19,8 +19,10 @@ def test_buckets_cover_corpus_once_and_respect_token_cap():
     idx = np.concatenate([b.index for b in bs])
     assert sorted(idx.tolist()) == list(range(len(srcs)))
     for b in bs:
-        assert b.tokens <= 8192
+        assert len(b.index) * max(lens[i] for i in b.index) <= 8192  # padded batch size (C5)
         assert b.tokens == sum(lens[i] for i in b.index)
+    # packed-token buckets are never smaller
+    assert len(P.length_buckets(lens, max_tokens=8192, padded=False)) <= len(bs)
     # buckets are length-sorted runs: lengths inside a bucket are contiguous in sorted order
     maxes = [max(lens[i] for i in b.index) for b in bs]
     mins = [min(lens[i] for i in b.index) for b in bs]
