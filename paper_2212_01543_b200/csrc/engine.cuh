@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -27,6 +28,7 @@
 #include "gemv_small.cuh"
 #include "kernels.cuh"
 #include "tc_gemm.cuh"
+#include "tc_gemm_ln.cuh"
 #include "tmap.h"
 
 #include "engine_iface.h"
@@ -707,11 +709,42 @@ struct Engine : EngineBase {
       if constexpr (!Epi::kRowWise && CL == 1) sk.splits = choose_splits(M, N, K, BN);
       // M: count, or upper bound with M_dev; CL = 2 works on vertical tile pairs
       const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL) * sk.splits;
-      const int grid = std::min(units, num_sms / CL) * CL;
+      const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
       launch_cluster = CL;
       launch(kern, grid, TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi, sk);
       launch_cluster = 1;
     }
+  }
+  // Clusters of CL CTAs (one per SM) that can be resident at once: a persistent grid
+  // larger than that would run its last clusters as a second wave. GPCs hold
+  // different SM counts, so this can be below num_sms / CL.
+  std::map<std::pair<const void*, int>, int> resident_cache;
+  template <class K>
+  int resident_clusters(K kern, int smem, int CL) {
+    if (CL == 1) return num_sms;
+    auto key = std::make_pair(reinterpret_cast<const void*>(kern), CL);
+    auto it = resident_cache.find(key);
+    if (it != resident_cache.end()) return it->second;
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(CL * (num_sms / CL));
+    c.blockDim = dim3(TC_THREADS);
+    c.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &c) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms / CL;
+    }
+    n = std::min(n, num_sms / CL);
+    resident_cache[key] = n;
+    if (getenv("HRT_DEBUG_CLUSTERS")) fprintf(stderr, "resident clusters of %d: %d\n", CL, n);
+    return n;
   }
   // CTA pairs sharing the weight tile (multicast) once there are enough row
   // tiles to pair up (large-batch encoder / Stage II / vocabulary GEMMs)
@@ -805,9 +838,45 @@ struct Engine : EngineBase {
   // GEMV path the last CTA normalises (no LN launch), else GEMM + LN kernel
   bool use_tail_ln = false;  // option "tail_ln" (measured slower than the separate LN launch: off)
   bool tail_ln_ok(int M, int K) const { return BF16 && use_tail_ln && gemv_ok(M, K) && d % 128 == 0 && d <= 1024; }
+  // residual + LayerNorm in the tcgen05 epilogue (tc_gemm_ln.cuh): rows above the GEMV
+  // regime, d a multiple of 256 with d / 256 in {1, 2, 4} (a cluster of d / 256 CTAs per row block)
+  bool use_ln_epi = false;  // option "ln_epi" (correct, measured slower than GEMM + LN kernel: off)
+  bool ln_epi_ok(int M, int K) const {
+    const int nc = d / TL_BN;
+    return BF16 && use_ln_epi && !gemv_ok(M, K) && d % TL_BN == 0 && (nc == 1 || nc == 2 || nc == 4) &&
+           K % TC_BK == 0;
+  }
+  template <int NC>
+  void resln_launch(const T* A, int a_cap, int lda, int M, const T* W, int K, const ResLnArgs& ra,
+                    const int* M_dev) {
+    if constexpr (BF16) {
+      constexpr int ST = 3;  // 3 x 48 KB ring + 32 KB transpose buffers + row statistics
+      auto kern = tc_gemm_resln_kernel<NC, ST>;
+      const int smem = TlSmem<NC, ST>::TOTAL;
+      smem_optin(kern, smem);
+      const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
+      const CUtensorMap& tb = tmap(W, d, K, K, TL_BN);
+      const int grid = std::min(cdiv(M, TC_BM), resident_clusters(kern, smem, NC)) * NC;
+      launch_cluster = NC;
+      launch(kern, grid, TC_THREADS, smem, ta, tb, M, K, M_dev, ra);
+      launch_cluster = 1;
+    }
+  }
+  // x += A W^T + bias, then y = LN(x) (rows out_row[r] of y when given): one fused
+  // launch on the tcgen05 path, GEMV tail-LN or GEMM + LN kernel otherwise
   void gemm_res_ln(const T* A, int a_cap, int lda, int M, const T* W, int K, float* x, const float* bias,
-                   const float* g, const float* b, T* y, const int* M_dev) {
+                   const float* g, const float* b, T* y, const int* M_dev, const int* out_row = nullptr) {
     if (M <= 0) return;
+    if (ln_epi_ok(M, K)) {
+      Scope sc(this, K_GEMM, (double)sizeof(T) * ((double)d * K + (double)M * K), 2.0 * M * d * K);
+      const ResLnArgs ra{x, d, bias, g, b, reinterpret_cast<bf16*>(y), d, out_row};
+      const int nc = d / TL_BN;
+      if (nc == 1) resln_launch<1>(A, a_cap, lda, M, W, K, ra, M_dev);
+      else if (nc == 2) resln_launch<2>(A, a_cap, lda, M, W, K, ra, M_dev);
+      else resln_launch<4>(A, a_cap, lda, M, W, K, ra, M_dev);
+      check_launch();
+      return;
+    }
     if (tail_ln_ok(M, K)) {
       Scope sc(this, K_GEMM, (double)sizeof(T) * ((double)d * K + (double)M * K), 2.0 * M * d * K);
       gemv_launch<false, true>(A, lda, M, W, d, K, EpiResidual{x, d, bias}, M_dev, GvLN{nullptr, nullptr, nullptr},
@@ -816,7 +885,7 @@ struct Engine : EngineBase {
       return;
     }
     gemm(K_GEMM, A, a_cap, lda, M, W, d, K, EpiResidual{x, d, bias}, M_dev);
-    layernorm(x, M, g, b, y, nullptr, nullptr, M_dev);
+    layernorm(x, M, g, b, y, out_row, nullptr, M_dev);
   }
   // LayerNorm feeding a projection: fused into the GEMV prologue on the
   // small-M path (bit-identical operand), else LN kernel + GEMM
@@ -1181,15 +1250,25 @@ struct Engine : EngineBase {
       if (!(sk & 2))
         attn_prefill(items, n_items, eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, off, len, len,
                      nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
+      // residual projections carry the next LayerNorm (fused epilogue on the tcgen05 path)
+      const float* ng = i + 1 < Le ? enc[i + 1].ln1g : enc_lng;
+      const float* nb = i + 1 < Le ? enc[i + 1].ln1b : enc_lnb;
+      if (sk == 0) {
+        gemm_res_ln(eb.ctx, Me_max, d, M, w.wo, d, eb.x, w.bo, w.ln2g, w.ln2b, eb.y, nullptr);
+        gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
+        if (i + 1 < Le || !p_mem_target) {
+          gemm_res_ln(eb.hid, Me_max, ff, M, w.w2, ff, eb.x, w.b2, ng, nb, eb.y, nullptr);
+        } else {  // protocol encode: the final LN also writes the fp32 memory
+          gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
+          layernorm(eb.x, M, enc_lng, enc_lnb, eb.y, nullptr, p_mem_target);
+        }
+        continue;
+      }
       if (!(sk & 4)) gemm(K_GEMM, eb.ctx, Me_max, d, M, w.wo, d, d, EpiResidual{eb.x, d, w.bo});
       if (!(sk & 1)) layernorm(eb.x, M, w.ln2g, w.ln2b, eb.y);
       if (!(sk & 4)) gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
       if (!(sk & 4)) gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
-      if (i + 1 < Le) {
-        if (!(sk & 1)) layernorm(eb.x, M, enc[i + 1].ln1g, enc[i + 1].ln1b, eb.y);
-      } else {
-        layernorm(eb.x, M, enc_lng, enc_lnb, eb.y, nullptr, p_mem_target);
-      }
+      if (!(sk & 1) || i + 1 == Le) layernorm(eb.x, M, ng, nb, eb.y, nullptr, i + 1 < Le ? nullptr : p_mem_target);
     }
     gemm(K_GEMM, eb.y, Me_max, d, M, wxkv, Ld * 2 * d, d, EpiBiasT<T, false>{xkv, Ld * 2 * d, bxkv});
   }
@@ -1218,7 +1297,9 @@ struct Engine : EngineBase {
       if (!(s1_skip & 2)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
                         nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd, hist2);
       // Wo + residual (+ LN2 in the GEMV tail on the small-row path)
-      const bool tail = tail_ln_ok(R, d) && !(s1_skip & 5);
+      // the LayerNorm after each residual projection rides in its epilogue: GEMV tail
+      // (option tail_ln) or the tcgen05 cluster epilogue (option ln_epi, rows above the GEMV regime)
+      const bool tail = (tail_ln_ok(R, d) || ln_epi_ok(R, d)) && !(s1_skip & 5);
       Tag _tg15(this, "s1.wo");
       if (tail)
         gemm_res_ln(s1.ctx, R_max, d, R, w.wo, d, s1.x, w.bo, w.ln2g, w.ln2b, s1.y, Rd);
@@ -1246,7 +1327,7 @@ struct Engine : EngineBase {
       // W2 + residual (+ the next LayerNorm: next layer's LN1 or the final LN)
       const float* ng = i + 1 < Ld ? dec[i + 1].ln1g : dec_lng;
       const float* nb = i + 1 < Ld ? dec[i + 1].ln1b : dec_lnb;
-      const bool tail2 = tail && tail_ln_ok(R, ff) && !(i + 1 == Ld && final_ln_fused);
+      const bool tail2 = tail && (tail_ln_ok(R, ff) || ln_epi_ok(R, ff)) && !(i + 1 == Ld && final_ln_fused);
       Tag _tg31(this, "s1.w2");
       if (tail2)
         gemm_res_ln(s1.hid, R_max, ff, R, w.w2, ff, s1.x, w.b2, ng, nb, s1.y, Rd);
@@ -1276,21 +1357,18 @@ struct Engine : EngineBase {
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s2.qkv, 3 * d, w.bqkv});
       attn_prefill(items, n_items, s2.qkv, 3 * d, s2.qkv + d, s2.qkv + 2 * d, 3 * d, s2.ctx, d, off, slot, qlen,
                    nullptr, off, qlen, key_ok, causal, 4.0 * d * (double)max_slot * M2);
-      gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.wo, d, d, EpiResidual{s2.x, d, w.bo});
-      layernorm(s2.x, M2, w.ln2g, w.ln2b, s2.y);
+      gemm_res_ln(s2.ctx, M2_max, d, M2, w.wo, d, s2.x, w.bo, w.ln2g, w.ln2b, s2.y, nullptr);
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.wqc, d, d, EpiBiasT<T, false>{s2.qc, d, w.bqc});
       attn_prefill(items, n_items, s2.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d,
                    s2.ctx, d, off, slot, qlen, kv_map, src_off, src_len, nullptr, 0, 4.0 * d * (double)max_src * M2);
-      gemm(K_GEMM, s2.ctx, M2_max, d, M2, w.woc, d, d, EpiResidual{s2.x, d, w.boc});
-      layernorm(s2.x, M2, w.ln3g, w.ln3b, s2.y);
+      gemm_res_ln(s2.ctx, M2_max, d, M2, w.woc, d, s2.x, w.boc, w.ln3g, w.ln3b, s2.y, nullptr);
       gemm(K_GEMM, s2.y, M2_max, d, M2, w.w1, ff, d, EpiBiasT<T, true>{s2.hid, ff, w.b1});
-      gemm(K_GEMM, s2.hid, M2_max, ff, M2, w.w2, d, ff, EpiResidual{s2.x, d, w.b2});
       if (i + 1 < Ld)
-        layernorm(s2.x, M2, dec[i + 1].ln1g, dec[i + 1].ln1b, s2.y);
-      else if (out_row)
-        layernorm(s2.x, M2, dec_lng, dec_lnb, s2.ymask, out_row);
+        gemm_res_ln(s2.hid, M2_max, ff, M2, w.w2, ff, s2.x, w.b2, dec[i + 1].ln1g, dec[i + 1].ln1b, s2.y, nullptr);
+      else if (out_row)  // only the [MASK] rows are normalised, gathered into the vocab operand
+        gemm_res_ln(s2.hid, M2_max, ff, M2, w.w2, ff, s2.x, w.b2, dec_lng, dec_lnb, s2.ymask, nullptr, out_row);
       else
-        layernorm(s2.x, M2, dec_lng, dec_lnb, s2.y);
+        gemm_res_ln(s2.hid, M2_max, ff, M2, w.w2, ff, s2.x, w.b2, dec_lng, dec_lnb, s2.y, nullptr);
     }
   }
 
@@ -1699,7 +1777,10 @@ struct Engine : EngineBase {
       attn_rows_mode = value;
       drop_loop_graphs();
     }
-    else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
+    else if (name == "ln_epi") {
+      use_ln_epi = value != 0;
+      drop_loop_graphs();
+    } else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
       if (name == "gemv_max_m") {
         if (value != 32 && value != 64 && value != 128) throw HrtError(HRT_ERR_INVALID, "gemv_max_m: 32, 64 or 128");
         gemv_max_m = value;

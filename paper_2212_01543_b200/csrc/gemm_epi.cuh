@@ -110,6 +110,29 @@ struct EpiResidual {
       }
     }
   }
+  // prefetching form (tcgen05 epilogue): the residual rows of a 32-column chunk are
+  // requested one chunk ahead, so their DRAM latency overlaps the previous chunk
+  static constexpr bool kPrefetch = true;
+  __device__ __forceinline__ void prefetch8(int row0, int col, int M, float4 (&p)[8]) const {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      p[i] = row0 + 4 * i < M ? *reinterpret_cast<const float4*>(x + (size_t)(row0 + 4 * i) * ldx + col)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ __forceinline__ void apply8_pre(int row0, int col, const float4* v, int M, const float4 (&prev)[8]) const {
+    const float4 b = *reinterpret_cast<const float4*>(bias + col);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (row0 + 4 * i < M) {
+        float4 a = prev[i];
+        a.x += v[i].x + b.x;
+        a.y += v[i].y + b.y;
+        a.z += v[i].z + b.z;
+        a.w += v[i].w + b.w;
+        *reinterpret_cast<float4*>(x + (size_t)(row0 + 4 * i) * ldx + col) = a;
+      }
+    }
+  }
   __device__ __forceinline__ void apply1(int row, int col, float v) const {
     x[(size_t)row * ldx + col] += v + bias[col];
   }

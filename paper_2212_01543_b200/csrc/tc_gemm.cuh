@@ -70,6 +70,16 @@ struct EpiRowStore<E, decltype(void(E::kRowStore))> {
   static constexpr bool value = E::kRowStore;
 };
 
+// element-wise epilogues whose global operands can be requested a chunk ahead (Epi::kPrefetch)
+template <class E, class = void>
+struct EpiPrefetch {
+  static constexpr bool value = false;
+};
+template <class E>
+struct EpiPrefetch<E, decltype(void(E::kPrefetch))> {
+  static constexpr bool value = E::kPrefetch;
+};
+
 // B (weight) tile load: whole BN-row box (CL = 1), or this CTA's BN/2-row
 // half multicast to both CTAs of the pair (CL = 2; the tensor map's box is BN/2 rows)
 template <int BN, int CL>
@@ -244,6 +254,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t aphase = (it >> 1) & 1;
       const int m0 = ((tile / n_tiles) * CL + crank) * TC_BM, n0 = (tile % n_tiles) * BN;
       const int rbase = m0 + quarter * 32;
+      constexpr bool PF = EpiPrefetch<Epi>::value && !Epi::kRowWise;
+      float4 pfa[PF ? 8 : 1];
+      // residual operands of the first chunk are requested before the accumulator is ready
+      if constexpr (PF) {
+        if (S == 1 && cbeg < cend && n0 + cbeg + (lane & 7) * 4 < N)
+          epi.prefetch8(rbase + (lane >> 3), n0 + cbeg + (lane & 7) * 4, M, pfa);
+      }
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -321,7 +338,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (S == 1) {
             // rows rbase + (lane >> 3) + 4 i; all global loads of the group are
             // issued before any store (memory-level parallelism)
-            if (col < N) epi.apply8(rbase + (lane >> 3), col, vals, M);
+            if constexpr (PF) {
+              float4 nxt[8];
+              const int ncol = col + 32;
+              if (c + 32 < cend && ncol < N) epi.prefetch8(rbase + (lane >> 3), ncol, M, nxt);
+              if (col < N) epi.apply8_pre(rbase + (lane >> 3), col, vals, M, pfa);
+              if (c + 32 < cend) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) pfa[i] = nxt[i];
+              }
+            } else {
+              if (col < N) epi.apply8(rbase + (lane >> 3), col, vals, M);
+            }
           } else if (col < N) {
             // split-K: this slice's fp32 partial tile
 #pragma unroll

@@ -565,6 +565,14 @@ def test_bf16_c2_shape_large_batch(hrt):
     b = eng.translate_batch(srcs, 2, max_steps=caps)
     for x, y in zip(a, b):
         assert x.tokens == y.tokens and x.score == y.score
+    # residual + LayerNorm fused into the tcgen05 epilogue (cluster of d / 256 CTAs exchanging
+    # row statistics over DSMEM): only the LN summation order differs from GEMM + LN kernel
+    eng.set_option("cluster", 1)
+    eng.set_option("ln_epi", 1)
+    e = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("ln_epi", 0)
+    same = sum(p == q for x, y in zip(a, e) for p, q in zip(x.tokens, y.tokens))
+    assert same / sum(max(len(x.tokens), len(y.tokens)) for x, y in zip(a, e)) > 0.98
     f32 = hrt.Engine(model, dtype="float32", max_sentences=len(srcs), max_beam=1)
     c = f32.translate_batch(srcs, 2, max_steps=caps)
     agree = total = 0

@@ -16,7 +16,7 @@ def load(path):
 
 def short(name):
     name = re.sub(r"\(.*", "", name)
-    m = re.match(r"(?:void )?(?:hrt::)?([\w:]+)(<.*>)?", name)
+    m = re.match(r"(?:void )?(?:hrt(?:_bf16|_f32)?::)?([\w:]+)(<.*>)?", name)
     base = m.group(1) if m else name
     tmpl = m.group(2) or ""
     for tag in ("VocabEpi", "EpiBiasT<[^>]*true>", "EpiBiasT", "EpiResidual", "EpiStoreF32"):
