@@ -678,6 +678,21 @@ struct Engine : EngineBase {
     return tmaps.emplace(key, make_tmap_bf16_kmajor(p, rows, cols, ld, box)).first->second;
   }
 
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps_out;
+  template <class Epi>
+  const CUtensorMap& tmap_out(const Epi& epi, int rows, int cols, const CUtensorMap& dummy) {
+    if constexpr (EpiTmaStore<Epi>::value) {
+      auto key = std::make_tuple(static_cast<const void*>(epi.out), rows, cols, epi.ldo);
+      auto it = tmaps_out.find(key);
+      if (it != tmaps_out.end()) return it->second;
+      return tmaps_out.emplace(key, make_tmap_bf16_store(epi.out, rows, cols, epi.ldo)).first->second;
+    } else {
+      (void)epi;
+      (void)rows;
+      (void)cols;
+      return dummy;
+    }
+  }
   // split-K workspace: fp32 partial tiles + per-tile arrival counters
   float* sk_ws = nullptr;
   int* sk_counters = nullptr;
@@ -705,13 +720,15 @@ struct Engine : EngineBase {
       smem_optin(kern, smem);
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN / CL);
+      // bf16 element-wise outputs leave through TMA tile stores (the buffer holds a_cap rows)
+      const CUtensorMap& tc = tmap_out<Epi>(epi, a_cap, N, ta);
       SplitK sk{1, sk_ws, sk_counters};
       if constexpr (!Epi::kRowWise && CL == 1) sk.splits = choose_splits(M, N, K, BN);
       // M: count, or upper bound with M_dev; CL = 2 works on vertical tile pairs
       const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL) * sk.splits;
       const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
       launch_cluster = CL;
-      launch(kern, grid, TC_THREADS, smem, ta, tb, M, N, K, M_dev, epi, sk);
+      launch(kern, grid, TC_THREADS, smem, ta, tb, tc, M, N, K, M_dev, epi, sk);
       launch_cluster = 1;
     }
   }

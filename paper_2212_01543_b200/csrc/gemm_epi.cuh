@@ -6,6 +6,8 @@
 //   EpiResidual        x += acc + b          (O-proj / FFN2 + residual, infer.py:204-205, :210-212)
 //   EpiStoreF32        logits = acc          (parity / debug logits)
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace hrt {
@@ -66,6 +68,24 @@ struct EpiBiasT {
     float a = v + bias[col];
     if (RELU) a = fmaxf(a, 0.f);
     out[(size_t)row * ldo + col] = from_f<T>(a);
+  }
+  // TMA-store form (tcgen05 epilogue, bf16 out): one row's 32 columns -> 16 packed bf16 pairs
+  static constexpr bool kTmaStore = std::is_same<T, bf16>::value;
+  __device__ __forceinline__ void row32_pack(int col0, const float* v, uint32_t* pk) const {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0) + j);
+      float a0 = v[4 * j] + b.x, a1 = v[4 * j + 1] + b.y, a2 = v[4 * j + 2] + b.z, a3 = v[4 * j + 3] + b.w;
+      if (RELU) {
+        a0 = fmaxf(a0, 0.f);
+        a1 = fmaxf(a1, 0.f);
+        a2 = fmaxf(a2, 0.f);
+        a3 = fmaxf(a3, 0.f);
+      }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
+      pk[2 * j] = *reinterpret_cast<uint32_t*>(&lo);
+      pk[2 * j + 1] = *reinterpret_cast<uint32_t*>(&hi);
+    }
   }
   // split form for latency-bound callers: every operand load issued before any store
   __device__ __forceinline__ float2 load2(int, int col) const { return make_float2(__ldg(bias + col), 0.f); }

@@ -70,6 +70,16 @@ struct EpiRowStore<E, decltype(void(E::kRowStore))> {
   static constexpr bool value = E::kRowStore;
 };
 
+// element-wise epilogues that write bf16 tiles with TMA stores (Epi::kTmaStore)
+template <class E, class = void>
+struct EpiTmaStore {
+  static constexpr bool value = false;
+};
+template <class E>
+struct EpiTmaStore<E, decltype(void(E::kTmaStore))> {
+  static constexpr bool value = E::kTmaStore;
+};
+
 // element-wise epilogues whose global operands can be requested a chunk ahead (Epi::kPrefetch)
 template <class E, class = void>
 struct EpiPrefetch {
@@ -101,8 +111,9 @@ __device__ __forceinline__ void tc_load_b(uint8_t* dst, const CUtensorMap* tmB, 
 // barrier counts one MMA-commit arrival from each CTA). Split-K is CL = 1 only.
 template <int BN, int STAGES, class Epi, int CL = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, const int* __restrict__ M_dev, Epi epi, SplitK sk) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, const int* __restrict__ M_dev, Epi epi,
+                   SplitK sk) {
   using L = TcSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -247,6 +258,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int cend = BN >= 64 ? cbeg + BN / 2 : (ew < 4 ? BN : 0);
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFFSET) + ew * (32 * TC_STG_LD);
     int it = 0;
+    int sc = 0;  // TMA-store staging buffers used by this warp (alternating halves of stg)
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     for (int u = cid; u < num_units; u += ncl, ++it) {
       const int tile = u / S, ks = u - tile * S;
@@ -298,6 +310,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         if (live) epi.end(st, row, n0 + cbeg);
+      } else if constexpr (EpiTmaStore<Epi>::value) {
+        // lane = row: bias (+ ReLU) -> bf16 -> this warp's 64-byte-swizzled 32 x 32 staging
+        // tile -> one TMA store per chunk (no register transpose, no per-lane global stores;
+        // rows past M inside the tile land in the buffer's spare rows or are clipped by TMA)
+        uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
+        uint32_t ra[32], rb[32];
+        if (cbeg < cend) tmem_ld32_issue(tbase + cbeg, ra);
+#pragma unroll 1
+        for (int c = cbeg; c < cend; c += 32) {
+          tmem_ld_wait(ra);
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
+          if (c + 32 < cend) tmem_ld32_issue(tbase + c + 32, rb);
+          const int col0 = n0 + c;
+          if (col0 < N) {
+            uint32_t pk[16];
+            epi.row32_pack(col0, v, pk);
+            uint8_t* buf = stg8 + (sc & 1) * 2048;
+            if (sc >= 2) {  // the store issued from this half two chunks ago has read it
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+            const uint32_t rowa = smem_u32(buf) + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + 16u * (j ^ ((lane >> 1) & 3))),
+                           "r"(pk[4 * j]), "r"(pk[4 * j + 1]), "r"(pk[4 * j + 2]), "r"(pk[4 * j + 3])
+                           : "memory");
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, buf, col0, rbase);
+              bulk_commit();
+            }
+            ++sc;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ra[i] = rb[i];
+        }
       } else if constexpr (EpiRowStore<Epi>::value) {
         // lane = row: the lane's 32 consecutive columns go out as full 64 / 128-byte
         // row segments (no shared-memory transpose)
@@ -401,6 +453,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if constexpr (EpiTmaStore<Epi>::value) {
+      if (lane == 0) bulk_wait_all();  // staged tiles fully written before the CTA retires
     }
   }
   tc_fence_before();

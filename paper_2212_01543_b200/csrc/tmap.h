@@ -39,4 +39,20 @@ inline CUtensorMap make_tmap_bf16_kmajor(const void* base, uint64_t rows, uint64
   return m;
 }
 
+// Output tile map for TMA stores: bf16 [rows, cols] with row stride `ld`,
+// 32 x 32 boxes (64-byte rows) in the 64-byte swizzle the epilogue writes.
+inline CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (store) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 }  // namespace hrt

@@ -90,7 +90,10 @@ double timeit(int M, int N, int K, const bf16* A, const bf16* B, const Epi& epi)
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto go = [&]() { cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr}); };
+  // output tile map for the TMA-store epilogue (EpiBiasT<bf16>); other epilogues ignore it
+  CUtensorMap tc = ta;
+  if constexpr (EpiTmaStore<Epi>::value) tc = make_tmap_bf16_store(epi.out, M, N, epi.ldo);
+  auto go = [&]() { cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr}); };
   for (int w = 0; w < 3; ++w) go();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);

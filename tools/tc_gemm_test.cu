@@ -72,7 +72,7 @@ bool run(int M, int N, int K) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto go = [&]() { CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr})); };
+  auto go = [&]() { CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, ta, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr})); };
   go();
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
@@ -149,7 +149,7 @@ void time_vocab(int M, int N, int K) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto go = [&]() { CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr})); };
+  auto go = [&]() { CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, ta, M, N, K, (const int*)nullptr, epi, SplitK{1, nullptr, nullptr})); };
   for (int w = 0; w < 3; ++w) go();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
