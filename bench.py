@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--sweep", default="", help="comma list of extra batch sizes to report")
     ap.add_argument("--streams", type=int, default=1, help="concurrent engines (CUDA streams) per GPU")
-    ap.add_argument("--pipeline", type=int, default=2,
+    ap.add_argument("--pipeline", type=int, default=4,
                     help="engines (CUDA streams) that consecutive batches are dealt to round-robin; the timed "
                          "region is the whole K-batch job (1: one batch at a time, L2 flushed between)")
     ap.add_argument("--corpus-streams", type=int, default=4, help="concurrent engines for the C5 corpus run")

@@ -27,6 +27,7 @@ def load(path):
 
 
 def klass(name):
+    name = re.sub(r"hrt(_bf16|_f32)?::", "", name).replace("(int)", "")
     base = re.sub(r"\(.*", "", name)
     m = re.search(r"tc_gemm_kernel<(\d+), (\d+), (\w+)", name)
     if m:
