@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 #include "tc_gemm.cuh"
 #include "tc_gemm_ln.cuh"
+#include "decode_cluster.cuh"
 #include "tmap.h"
 
 #include "engine_iface.h"
@@ -1636,6 +1637,74 @@ struct Engine : EngineBase {
     return bs;
   }
 
+  // Stage-I decoder layers of <= 4 greedy rows on one 16-CTA cluster (decode_cluster.cuh)
+  int cluster_decode_mode = 1;  // option "cluster_decode": 1 auto (d 512, ff 2048, 8 heads), 0 off
+  int cluster_decode_state = -1;  // -1 unknown, 0 unavailable on this device, 1 available
+  int dc_dbg = 0;                 // option "dc_dbg" (timing attribution only)
+  bool cluster_decode_ok(int R) {
+    if constexpr (!BF16) return false;
+    const int Rp = path_rows > 0 ? path_rows : R;
+    // mode 1 (default): single-row buckets, where the cluster kernel measured faster than the
+    // per-kernel chain (33.1 vs 34.7 us per batch-1 step); mode 2: buckets up to 4 rows
+    const int rmax = cluster_decode_mode >= 2 ? DC_RMAX : 1;
+    if (!cluster_decode_mode || d != DC_D || ff != DC_FF || H != DC_H || Ld > DC_MAXL || Rp > rmax || s1_skip ||
+        ln_fusable(R))
+      return false;
+    if (cluster_decode_state < 0) {
+      auto prep = [&](auto kern) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DcSmem::TOTAL) != cudaSuccess)
+          return false;
+        cudaLaunchConfig_t c = {};
+        c.gridDim = dim3(DC_CN);
+        c.blockDim = dim3(DC_THREADS);
+        c.dynamicSmemBytes = DcSmem::TOTAL;
+        int n = 0;
+        return cudaOccupancyMaxActiveClusters(&n, kern, &c) == cudaSuccess && n >= 1;
+      };
+      const bool ok = prep(decode_cluster_kernel<1>) && prep(decode_cluster_kernel<2>) &&
+                      prep(decode_cluster_kernel<4>);
+      cudaGetLastError();
+      cluster_decode_state = ok ? 1 : 0;
+    }
+    return cluster_decode_state == 1;
+  }
+  void launch_decode_cluster(int R, int t, const int* src_off, const int* src_len, const StepCtl* ctl) {
+    DcParams dp{};
+    for (int i = 0; i < Ld; ++i) {
+      const DecW& w = dec[i];
+      auto b = [](const T* q) { return reinterpret_cast<const bf16*>(q); };
+      dp.L[i] = DcLayer{b(w.wqkv), b(w.wo), b(w.wqc), b(w.woc), b(w.w1), b(w.w2), w.bqkv, w.bo, w.bqc, w.boc, w.b1,
+                        w.b2, w.ln2g, w.ln2b, w.ln3g, w.ln3b, i + 1 < Ld ? dec[i + 1].ln1g : dec_lng,
+                        i + 1 < Ld ? dec[i + 1].ln1b : dec_lnb};
+    }
+    dp.Ld = Ld;
+    dp.xkv = reinterpret_cast<const bf16*>(xkv);
+    dp.xstride = Ld * 2 * d;
+    dp.src_off = src_off;
+    dp.src_len = src_len;
+    dp.kc = reinterpret_cast<bf16*>(s1.kc);
+    dp.vc = reinterpret_cast<bf16*>(s1.vc);
+    dp.cap = cap_max;
+    dp.rcap = R_max;
+    dp.x = s1.x;
+    dp.y = reinterpret_cast<bf16*>(s1.y);
+    dp.ctl = ctl;
+    dp.R_host = R;
+    dp.t_host = t;
+    dp.att_scale = att_scale;
+    dp.dbg = dc_dbg;
+    Scope sc(this, K_GEMM | K_ATTN, 2.0 * Ld * (6.0 * d * d + 2.0 * d * ff), 2.0 * R * Ld * (6.0 * d * d + 2.0 * d * ff));
+    const int Rp = path_rows > 0 ? path_rows : R;
+    if (Rp <= 1)
+      launch(decode_cluster_kernel<1>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+    else if (Rp <= 2)
+      launch(decode_cluster_kernel<2>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+    else
+      launch(decode_cluster_kernel<4>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+    check_launch();
+  }
+
   // One Stage-I step for R live rows (R is an upper bound when ctl != null):
   // decoder layers, vocab statistics, selection (greedy or beam), which also
   // embeds the next step's inputs.
@@ -1646,8 +1715,13 @@ struct Engine : EngineBase {
       const bool fuse = ln_fusable(R) && !(s1_skip & 1);  // final LN inside the vocab GEMV
       greedy_hist_identity = true;  // greedy rows never reorder: slot j of row r is row r
       try {
-        decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false, nullptr,
-                     fuse);
+        if (cluster_decode_ok(R)) {
+          Tag _tgc(this, "s1.decoder_cluster");
+          launch_decode_cluster(R, t, src_off, src_len, ctl);
+        } else {
+          decoder_step(R, t, t * k, cap_max, s_feed, s_hist, nullptr, src_off, src_len, max_src, ctl, false, nullptr,
+                       fuse);
+        }
       } catch (...) {
         greedy_hist_identity = false;
         throw;
@@ -1794,7 +1868,13 @@ struct Engine : EngineBase {
       attn_rows_mode = value;
       drop_loop_graphs();
     }
-    else if (name == "ln_epi") {
+    else if (name == "dc_dbg") {
+      dc_dbg = value;
+      drop_loop_graphs();
+    } else if (name == "cluster_decode") {
+      cluster_decode_mode = value;
+      drop_loop_graphs();
+    } else if (name == "ln_epi") {
       use_ln_epi = value != 0;
       drop_loop_graphs();
     } else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
