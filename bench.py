@@ -86,6 +86,17 @@ def workload(args, rank, step):
     return spec, k, srcs, caps
 
 
+def config_of(args, spec, k, ws):
+    """The workload / config block both arms print (identical strings, so the two lines
+    name the same benchmark; how each arm runs it is described outside `config`)."""
+    sh, b_at, B = spec["shape"], spec["beam"], args.batch
+    return {"workload": f"{args.config}: HRT k={k} {'greedy' if b_at == 1 else f'beam {b_at} (b_nat 1)'}, "
+                        f"E{sh.enc_layers}D{sh.dec_layers} d{sh.d_model} V{sh.vocab_size}, batch {B} "
+                        f"sentences/GPU/step, lengths {spec['lengths']}, Zipf(1.1) ids, random N(0,0.02) weights "
+                        f"seed {spec['seed']}, Stage-I cap ceil(floor(1.2 n + 10) / k)",
+            "batch_per_gpu": B, "k": k, "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"}
+
+
 def target_words(out, B):
     return int(np.asarray(out["lens"][:B]).sum())
 
@@ -272,8 +283,10 @@ def run_reference(args):
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.fmean(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: HRT k={k} greedy (reference CPU path, fp32)",
-                       "batch_per_gpu": args.batch, "k": k},
+            "config": config_of(args, spec, k, 1),
+            "method": "the reference's CPU algorithm (oracle port of infer.py / decoding.py), fp32 numpy with all "
+                      "host BLAS threads, sequential per sentence (the reference has no batched path), on a bounded "
+                      "sample of the benchmark batch",
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
                              "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -935,15 +948,10 @@ def run_engine(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": spec["dtype"], "data": "synthetic",
-        "config": {"workload": f"{args.config}: HRT k={k} {'greedy' if b_at == 1 else f'beam {b_at} (b_nat 1)'}, "
-                               f"E{sh.enc_layers}D{sh.dec_layers} d{sh.d_model} "
-                               f"V{sh.vocab_size}, batch {B} sentences/GPU/step, lengths {spec['lengths']}, "
-                               f"Zipf(1.1) ids, random N(0,0.02) weights seed {spec['seed']}",
-                   "batch_per_gpu": B, "k": k,
-                   "l2": (pipe_info["mode"] if pipe_info else "512 MiB flush between timed steps (outside events)"),
+        "config": config_of(args, spec, k, ws),
+        "method": {"l2": (pipe_info["mode"] if pipe_info else "512 MiB flush between timed steps (outside events)"),
                    "streams": S, "scheduling": f"batch cut into {S} length buckets, one engine/CUDA stream each, "
-                                               "run concurrently (no inter-stream communication)",
-                   "parallelism": f"dp{ws} (sentence shards, no collective in the decode loop)"},
+                                               "run concurrently (no inter-stream communication)"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e_tot / args.steps},
         "gpu_launches": launches, "gpu_launches_per_step": launches // max(1, args.steps),
