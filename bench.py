@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--corpus-sentences", type=int, default=200000)
     ap.add_argument("--no-corpus", action="store_true", help="skip the C5 corpus block of the default line")
     ap.add_argument("--no-at", action="store_true", help="skip the AT-baseline block")
+    ap.add_argument("--engine-opt", default="", help="engine options for every engine: name=value,...")
     ap.add_argument("--parity-seconds", type=float, default=10.0,
                     help="budget of the teacher-forced bf16 parity sample (fp64 oracle)")
     return ap.parse_args()
@@ -84,6 +85,13 @@ def workload(args, rank, step):
     srcs = W.make_sources(args.batch, seed, spec["lengths"])
     caps = W.stage1_caps(srcs, k)
     return spec, k, srcs, caps
+
+
+def apply_opts(args, engs):
+    for kv in [x for x in args.engine_opt.split(",") if x]:
+        name, val = kv.split("=")
+        for e in engs:
+            e.set_option(name, int(val))
 
 
 def config_of(args, spec, k, ws):
@@ -632,6 +640,7 @@ def run_engine(args):
     engs = [hrt.Engine(model, dtype="bfloat16" if spec["dtype"] == "bf16" else "float32", device=local,
                        max_sentences=per, max_beam=b_at) for _ in range(S)]
     eng = engs[0]
+    apply_opts(args, engs)
     del model
 
     batches = [workload(args, rank, s) for s in range(args.warmup + args.steps)]
@@ -760,6 +769,7 @@ def run_engine(args):
         pengs = [eng] + [hrt.Engine(hrt.HRTModel.random(sh, spec["seed"]), dtype="bfloat16" if spec["dtype"] == "bf16"
                                     else "float32", device=local, max_sentences=B, max_beam=b_at)
                          for _ in range(P - 1)]
+        apply_opts(args, pengs)
         pstreams = [stream] + [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local))
                                for e in pengs[1:]]
         pipe = Pipeline(torch, pengs, pstreams, batches, k, b_at, pin)

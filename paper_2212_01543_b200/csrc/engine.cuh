@@ -1093,6 +1093,13 @@ struct Engine : EngineBase {
                    double bytes, const int* t_dev = nullptr, const int* R_dev = nullptr, const int* hist2 = nullptr) {
     if (R <= 0) return;
     Scope sc(this, K_ATTN, bytes, 0.0);
+    // debug option "attn_pdl" = 0: decode attention launched without the programmatic edge
+    struct PdlScope {
+      bool& f;
+      bool old;
+      PdlScope(bool& flag, bool v) : f(flag), old(flag) { f = v; }
+      ~PdlScope() { f = old; }
+    } pdl_scope(pdl, pdl && attn_pdl);
     if constexpr (BF16) {
       // large row counts only (few rows: the warp-per-(row, head) kernel spreads wider); the
       // choice follows the graph's row bucket so graph and eager runs match bit for bit
@@ -1312,7 +1319,7 @@ struct Engine : EngineBase {
       Tag _tg10(this, "s1.qkv");
       if (!(s1_skip & 4)) gemm(K_GEMM, s1.y, R_max, d, R, w.wqkv, 3 * d, d, EpiBiasT<T, false>{s1.qkv, 3 * d, w.bqkv}, Rd);
       Tag _tg12(this, "s1.attn_self");
-      if (!(s1_skip & 2)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
+      if (!(s1_skip & 66)) attn_decode<true>(s1.qkv, 3 * d, s1.qkv + d, s1.qkv + 2 * d, 3 * d, kc, vc, hist, cap, t, nullptr, nullptr,
                         nullptr, R, cap, s1.ctx, 2.0 * sizeof(T) * (double)R * (t + 1) * d, td, Rd, hist2);
       // Wo + residual (+ LN2 in the GEMV tail on the small-row path)
       // the LayerNorm after each residual projection rides in its epilogue: GEMV tail
@@ -1329,7 +1336,7 @@ struct Engine : EngineBase {
       else if (!(s1_skip & 4))
         gemm_ln(K_GEMM, s1.x, w.ln2g, w.ln2b, s1.y, R_max, R, w.wqc, d, EpiBiasT<T, false>{s1.qc, d, w.bqc}, Rd);
       Tag _tg21(this, "s1.attn_cross");
-      if (!(s1_skip & 2)) attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
+      if (!(s1_skip & 130)) attn_decode<false>(s1.qc, d, xkv + (size_t)2 * i * d, xkv + (size_t)(2 * i + 1) * d, Ld * 2 * d, nullptr,
                          nullptr, nullptr, 0, 0, row_seq, kv_off, kv_len, R, max_src, s1.ctx,
                          2.0 * sizeof(T) * (double)R * max_src * d, nullptr, Rd);
       Tag _tg25(this, "s1.woc");
@@ -1641,6 +1648,7 @@ struct Engine : EngineBase {
   int cluster_decode_mode = 1;  // option "cluster_decode": 1 auto (d 512, ff 2048, 8 heads), 0 off
   int cluster_decode_state = -1;  // -1 unknown, 0 unavailable on this device, 1 available
   int dc_dbg = 0;                 // option "dc_dbg" (timing attribution only)
+  bool attn_pdl = true;           // option "attn_pdl" (debug)
   bool cluster_decode_ok(int R) {
     if constexpr (!BF16) return false;
     const int Rp = path_rows > 0 ? path_rows : R;
@@ -1868,7 +1876,10 @@ struct Engine : EngineBase {
       attn_rows_mode = value;
       drop_loop_graphs();
     }
-    else if (name == "dc_dbg") {
+    else if (name == "attn_pdl") {
+      attn_pdl = value != 0;
+      drop_loop_graphs();
+    } else if (name == "dc_dbg") {
       dc_dbg = value;
       drop_loop_graphs();
     } else if (name == "cluster_decode") {
@@ -2140,7 +2151,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     cur = (cur + trunc_off[B] + 7) & ~size_t(7);
   }
   {  // fixed header: loop control + alive[] + source offsets/lengths
-    StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, B, 0, 0};
+    // (timing attribution with kernels skipped produces garbage that may end rows early: the
+    // early exit is disabled then, so every step still runs)
+    StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, s1_skip ? (1 << 30) : B, 0, 0};
     std::memcpy(h_meta, &c, sizeof(StepCtl));
     int* ha = h_meta + 8;
     for (int t = 0; t <= cap_max; ++t) ha[t] = t < max_cap ? alive[t] : 0;

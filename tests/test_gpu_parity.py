@@ -106,6 +106,15 @@ def test_reorder_continues_from_parent_rows(hrt, golden):
     sess.step(c2, [8], 1)
     ref = sess.step(c2, [9], 2)
     assert np.abs(after[0] - ref[0]).max() < 1e-5
+    # and against the fp64 oracle's own reorder (infer.py:307-318)
+    orc = _oracle(g, _model(hrt, g))
+    orc.encode(src)
+    oc = orc.start_cache(2, 6)
+    orc.step(oc, [1, 1], 0)
+    orc.step(oc, [7, 8], 1)
+    orc.reorder(oc, [1, 1])
+    want = orc.step(oc, [9, 9], 2)
+    assert _rel(after, want) < REL
 
 
 def _check_translation(tr, ref, rel=REL):

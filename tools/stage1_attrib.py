@@ -9,13 +9,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--batches", default="1,64,1024")
 ap.add_argument("--steps", type=int, default=30)
+ap.add_argument("--opts", default="", help="engine options name=value,...")
 a = ap.parse_args()
 spec = W.CONFIGS[a.config]
 Bs = [int(x) for x in a.batches.split(",")]
 eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat16", max_sentences=max(Bs),
                  max_beam=spec["beam"])
+for kv in [x for x in a.opts.split(",") if x]:
+    kk, vv = kv.split("=")
+    eng.set_option(kk, int(vv))
 names = ((0, "full"),) if os.environ.get("FULL_ONLY") else ((0, "full"), (1, "-LN"), (4, "-gemm"), (8, "-vocab"), (16, "-select/rowstat"),
-         (32, "-embed/beam_sel"), (2, "-attn"))
+         (32, "-embed/beam_sel"), (2, "-attn"), (64, "-self-attn"), (128, "-cross-attn"))
 for B in Bs:
     srcs = W.make_sources(B, 1001, spec["lengths"])
     caps = [a.steps] * B
