@@ -818,9 +818,13 @@ struct Engine : EngineBase {
     }
     return true;
   }
+  // row-blocked GEMV (blockIdx.y = 64-row blocks) up to gemv_rows rows: at these row counts
+  // the tcgen05 tile pipeline is pure fixed latency (option "gemv_rows", 0 = off)
+  int gemv_rows = 128;  // measured: R = 128 step 71.4 -> 61.2 us; no gain at 256, slower at 512
   bool gemv_ok(int M, int K) const {
     const int Mp = path_rows > 0 ? path_rows : M;
-    return use_gemv && Mp <= gemv_max_m && K % 32 == 0 && (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
+    return use_gemv && Mp <= std::max(gemv_max_m, gemv_rows) && K % 32 == 0 &&
+           (K <= 512 || (K / 32) % GV_WARPS == 0) && K <= 4096;
   }
   // the vocabulary GEMV keeps per-row statistics in registers: at most 32 rows
   bool gemv_vocab_ok(int M) const {
@@ -830,8 +834,11 @@ struct Engine : EngineBase {
   template <int NT, int CPW, bool LNA, bool TLN, class Epi>
   void gemv_launch_t(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
                      const GvLN& ln, const GvTailLN& tln) {
-    launch(gemv_small_kernel<NT, CPW, Epi, LNA, TLN>, cdiv(N, 16), GV_THREADS, 0, reinterpret_cast<const bf16*>(A),
-           lda, reinterpret_cast<const bf16*>(frag_of(W)), N, K, M, M_dev, epi, ln, tln);
+    const int ry = cdiv(M, 8 * NT);  // 64-row blocks beyond 64 rows (NT = 8)
+    if (ry > 1 && (LNA || TLN)) throw HrtError(HRT_ERR_INVALID, "GEMV LayerNorm fusion needs <= 64 rows");
+    launch(gemv_small_kernel<NT, CPW, Epi, LNA, TLN>, dim3(cdiv(N, 16), ry), GV_THREADS, 0,
+           reinterpret_cast<const bf16*>(A), lda, reinterpret_cast<const bf16*>(frag_of(W)), N, K, M, M_dev, epi, ln,
+           tln);
   }
   template <int NT, bool LNA, bool TLN, class Epi>
   void gemv_launch_n(const T* A, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev,
@@ -849,13 +856,16 @@ struct Engine : EngineBase {
     if (M <= 8) gemv_launch_n<1, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
     else if (M <= 16) gemv_launch_n<2, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
     else if (M <= 32) gemv_launch_n<4, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
-    else if (M <= 64) gemv_launch_n<8, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
+    else if (M <= 64 || gemv_max_m <= 64) gemv_launch_n<8, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
     else gemv_launch_n<16, LNA, TLN>(A, lda, M, W, N, K, epi, M_dev, ln, tln);
   }
   // residual projection followed by a LayerNorm of the updated rows: on the
   // GEMV path the last CTA normalises (no LN launch), else GEMM + LN kernel
   bool use_tail_ln = false;  // option "tail_ln" (measured slower than the separate LN launch: off)
-  bool tail_ln_ok(int M, int K) const { return BF16 && use_tail_ln && gemv_ok(M, K) && d % 128 == 0 && d <= 1024; }
+  bool tail_ln_ok(int M, int K) const {
+    const int Mp = path_rows > 0 ? path_rows : M;
+    return BF16 && use_tail_ln && Mp <= 64 && gemv_ok(M, K) && d % 128 == 0 && d <= 1024;
+  }
   // residual + LayerNorm in the tcgen05 epilogue (tc_gemm_ln.cuh): rows above the GEMV
   // regime, d a multiple of 256 with d / 256 in {1, 2, 4} (a cluster of d / 256 CTAs per row block)
   bool use_ln_epi = false;  // option "ln_epi" (correct, measured slower than GEMM + LN kernel: off)
@@ -1887,6 +1897,10 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "ln_epi") {
       use_ln_epi = value != 0;
+      drop_loop_graphs();
+    } else if (name == "gemv_rows") {
+      if (value < 0 || value > 1024) throw HrtError(HRT_ERR_INVALID, "gemv_rows: 0 .. 1024");
+      gemv_rows = value;
       drop_loop_graphs();
     } else if (name == "ln_fuse" || name == "gemv" || name == "gemv_max_m") {
       if (name == "gemv_max_m") {

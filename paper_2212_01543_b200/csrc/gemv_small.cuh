@@ -204,6 +204,8 @@ __device__ __forceinline__ void gv_tail_ln(const float* x, int M, int K, const G
   if (threadIdx.x == 0) *t.counter = 0;  // re-arm for the next launch / graph replay
 }
 
+// Row blocks: blockIdx.y takes rows 8 NT y .. 8 NT (y + 1) - 1 (one weight pass per row
+// block; the weights are L2-resident), so one launch covers up to gridDim.y x 8 NT rows.
 template <int NT, int CPW, class Epi, bool LNA = false, bool TLN = false>
 __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ W, int N, int K, int M,
@@ -213,6 +215,9 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
   __shared__ float red[GV_WARPS][NG * 4][32];
   __shared__ float2 lnst[LNA ? 8 * NT : 1];
   pdl_trigger();
+  const int rb0 = blockIdx.y * 8 * NT;  // first row of this row block (0 without row blocking)
+  A += (size_t)rb0 * lda;
+  M -= rb0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
   const int n0 = blockIdx.x * 16;
   const int nch = K / 32;  // == GV_WARPS * CPW, or fewer chunks than warps with CPW == 1
@@ -248,8 +253,8 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
                                                                   32 * (c0 + i) + t4 * 8)
                                : make_uint4(0, 0, 0, 0);
   }
-  if (M_dev) M = *M_dev;
-  if (M <= 0) return;  // every Stage-I row finished (uniform across the CTA)
+  if (M_dev) M = *M_dev - rb0;
+  if (M <= 0) return;  // every Stage-I row finished / no live row in this block (uniform across the CTA)
   // The final reduction and epilogue are spread over NG warps: warp w < NG owns
   // n-tiles w, w + NG, ...; its epilogue operands (residual rows, bias) are
   // issued now and consumed after the reduction.
@@ -264,10 +269,10 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
       const int r0 = 8 * j + 2 * t4;
       const int ra = min(r0, M - 1), rb = min(r0 + 1, M - 1);
       const int fa = min(f0, N - 1), fb = min(f1, N - 1);
-      pre[o][0] = epi.load2(ra, fa);
-      pre[o][1] = epi.load2(rb, fa);
-      pre[o][2] = epi.load2(ra, fb);
-      pre[o][3] = epi.load2(rb, fb);
+      pre[o][0] = epi.load2(rb0 + ra, fa);
+      pre[o][1] = epi.load2(rb0 + rb, fa);
+      pre[o][2] = epi.load2(rb0 + ra, fb);
+      pre[o][3] = epi.load2(rb0 + rb, fb);
     }
   }
   if (LNA) {
@@ -323,12 +328,12 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_small_kernel(const bf16* __re
       const int j = o * NG + warp;
       const int r0 = 8 * j + 2 * t4;
       if (r0 < M) {
-        if (f0 < N) epi.store2(r0, f0, fin[o][0], pre[o][0]);
-        if (f1 < N) epi.store2(r0, f1, fin[o][2], pre[o][2]);
+        if (f0 < N) epi.store2(rb0 + r0, f0, fin[o][0], pre[o][0]);
+        if (f1 < N) epi.store2(rb0 + r0, f1, fin[o][2], pre[o][2]);
       }
       if (r0 + 1 < M) {
-        if (f0 < N) epi.store2(r0 + 1, f0, fin[o][1], pre[o][1]);
-        if (f1 < N) epi.store2(r0 + 1, f1, fin[o][3], pre[o][3]);
+        if (f0 < N) epi.store2(rb0 + r0 + 1, f0, fin[o][1], pre[o][1]);
+        if (f1 < N) epi.store2(rb0 + r0 + 1, f1, fin[o][3], pre[o][3]);
       }
     }
   }
