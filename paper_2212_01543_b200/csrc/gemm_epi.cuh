@@ -69,8 +69,24 @@ struct EpiBiasT {
     if (RELU) a = fmaxf(a, 0.f);
     out[(size_t)row * ldo + col] = from_f<T>(a);
   }
-  // TMA-store form (tcgen05 epilogue, bf16 out): one row's 32 columns -> 16 packed bf16 pairs
+  // TMA-store form (tcgen05 epilogue, bf16 out): one row's 32 columns -> 16 packed bf16 pairs.
+  // bias_lane = bias[col0 + lane] (one coalesced load per chunk, requested a chunk ahead);
+  // column j's bias is broadcast from lane j by a shuffle
   static constexpr bool kTmaStore = std::is_same<T, bf16>::value;
+  __device__ __forceinline__ float bias_of(int col) const { return __ldg(bias + col); }
+  __device__ __forceinline__ void row32_pack_shfl(float bias_lane, const float* v, uint32_t* pk) const {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float a0 = v[2 * j] + __shfl_sync(0xffffffffu, bias_lane, 2 * j);
+      float a1 = v[2 * j + 1] + __shfl_sync(0xffffffffu, bias_lane, 2 * j + 1);
+      if (RELU) {
+        a0 = fmaxf(a0, 0.f);
+        a1 = fmaxf(a1, 0.f);
+      }
+      __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+      pk[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  }
   __device__ __forceinline__ void row32_pack(int col0, const float* v, uint32_t* pk) const {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
         uint32_t ra[32], rb[32];
         if (cbeg < cend) tmem_ld32_issue(tbase + cbeg, ra);
+        float bcur = (cbeg < cend && n0 + cbeg + lane < N) ? epi.bias_of(n0 + cbeg + lane) : 0.f;
 #pragma unroll 1
         for (int c = cbeg; c < cend; c += 32) {
           tmem_ld_wait(ra);
@@ -324,10 +325,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
           if (c + 32 < cend) tmem_ld32_issue(tbase + c + 32, rb);
+          const float bnext = (c + 32 < cend && n0 + c + 32 + lane < N) ? epi.bias_of(n0 + c + 32 + lane) : 0.f;
           const int col0 = n0 + c;
           if (col0 < N) {
             uint32_t pk[16];
-            epi.row32_pack(col0, v, pk);
+            epi.row32_pack_shfl(bcur, v, pk);
             uint8_t* buf = stg8 + (sc & 1) * 2048;
             if (sc >= 2) {  // the store issued from this half two chunks ago has read it
               if (lane == 0) bulk_wait_read<1>();
@@ -347,6 +349,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             ++sc;
           }
+          bcur = bnext;
 #pragma unroll
           for (int i = 0; i < 32; ++i) ra[i] = rb[i];
         }
