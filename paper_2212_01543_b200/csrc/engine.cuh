@@ -1281,7 +1281,11 @@ struct Engine : EngineBase {
     const int sk = enc_skip;  // debug attribution: 1 LN, 2 attention, 4 projections (wrong results)
     for (int i = 0; i < Le; ++i) {
       const EncW& w = enc[i];
-      if (!(sk & 4)) gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
+      if (!(sk & 4)) {
+        Tag _t(this, "encoder.qkv");
+        gemm(K_GEMM, eb.y, Me_max, d, M, w.wqkv, 3 * d, d, EpiBiasT<T, false>{eb.qkv, 3 * d, w.bqkv});
+      }
+      Tag _ta(this, "encoder.attn");
       if (!(sk & 2))
         attn_prefill(items, n_items, eb.qkv, 3 * d, eb.qkv + d, eb.qkv + 2 * d, 3 * d, eb.ctx, d, off, len, len,
                      nullptr, off, len, nullptr, 0, 4.0 * d * (double)max_len_seq * M);
@@ -1289,9 +1293,16 @@ struct Engine : EngineBase {
       const float* ng = i + 1 < Le ? enc[i + 1].ln1g : enc_lng;
       const float* nb = i + 1 < Le ? enc[i + 1].ln1b : enc_lnb;
       if (sk == 0) {
-        gemm_res_ln(eb.ctx, Me_max, d, M, w.wo, d, eb.x, w.bo, w.ln2g, w.ln2b, eb.y, nullptr);
-        gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
+        {
+          Tag _t(this, "encoder.wo+ln");
+          gemm_res_ln(eb.ctx, Me_max, d, M, w.wo, d, eb.x, w.bo, w.ln2g, w.ln2b, eb.y, nullptr);
+        }
+        {
+          Tag _t(this, "encoder.w1");
+          gemm(K_GEMM, eb.y, Me_max, d, M, w.w1, ff, d, EpiBiasT<T, true>{eb.hid, ff, w.b1});
+        }
         if (i + 1 < Le || !p_mem_target) {
+          Tag _t(this, "encoder.w2+ln");
           gemm_res_ln(eb.hid, Me_max, ff, M, w.w2, ff, eb.x, w.b2, ng, nb, eb.y, nullptr);
         } else {  // protocol encode: the final LN also writes the fp32 memory
           gemm(K_GEMM, eb.hid, Me_max, ff, M, w.w2, d, ff, EpiResidual{eb.x, d, w.b2});
