@@ -66,6 +66,8 @@ typedef struct hrt_stats {
   int64_t arena_bytes;       /* device activation arena capacity (hrt_estimate_arena max) */
   int64_t arena_high_water;  /* largest phase footprint any call needed (<= arena_bytes) */
   int64_t weight_bytes;      /* device weight blob */
+  int64_t stage1_row_steps;  /* Stage-I rows computed, summed over steps (captured-graph loop, host I/O
+                                calls): below sum(cap) once rows stop at a natural EOS */
 } hrt_stats;
 
 /* Create an engine on `device`. `params` holds every parameter as fp32, in

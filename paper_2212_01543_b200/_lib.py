@@ -33,7 +33,8 @@ class HrtConfig(C.Structure):
 
 class HrtStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
-        "kernel_launches", "decoder_calls", "arena_bytes", "arena_high_water", "weight_bytes")]
+        "kernel_launches", "decoder_calls", "arena_bytes", "arena_high_water", "weight_bytes",
+        "stage1_row_steps")]
 
 
 class HrtTranslateOut(C.Structure):

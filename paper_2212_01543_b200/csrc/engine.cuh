@@ -118,6 +118,8 @@ struct Engine : EngineBase {
   double* o_scores;
   unsigned char* o_forced;
   int* h_meta = nullptr;  // pinned staging for per-call metadata (one H2D copy)
+  StepCtl* h_ctl = nullptr;  // pinned copy of the loop control after a call (row statistics)
+  bool unrolled_last = false;
   char* h_out = nullptr;  // pinned staging for the packed per-call outputs (one D2H copy)
   size_t h_out_bytes = 0;
   int meta_cap;
@@ -201,6 +203,7 @@ struct Engine : EngineBase {
     cudaFree(sk_counters);
     cudaFree(gv_counter);
     if (h_meta) cudaFreeHost(h_meta);
+    if (h_ctl) cudaFreeHost(h_ctl);
     if (h_out) cudaFreeHost(h_out);
     drop_loop_graphs();
     if (meta_ev) cudaEventDestroy(meta_ev);
@@ -663,6 +666,7 @@ struct Engine : EngineBase {
       CUDA_OK(cudaMemset(gv_counter, 0, 64 * sizeof(int)));
     }
     CUDA_OK(cudaMallocHost(&h_meta, (size_t)meta_cap * sizeof(int)));
+    CUDA_OK(cudaMallocHost(&h_ctl, sizeof(StepCtl)));
     h_out_bytes = (size_t)Bmax * Lmax * sizeof(int) + 2 * (size_t)Bmax * sizeof(int) + 8 + (size_t)Bmax * 3 * sizeof(double) + Bmax;
     CUDA_OK(cudaMallocHost(&h_out, h_out_bytes));
     CUDA_OK(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming));
@@ -1803,7 +1807,7 @@ struct Engine : EngineBase {
     try {
       for (int u = 0; u < U; ++u) {
         stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
-        launch(stage1_advance_plain_kernel, 1, 1, 0, s_ctl, s_alive);
+        launch(stage1_advance_plain_kernel, 1, 256, 0, s_ctl, s_alive, beam == 1 ? (const int*)s_done : nullptr);
         check_launch();
       }
     } catch (...) {
@@ -2178,7 +2182,8 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   {  // fixed header: loop control + alive[] + source offsets/lengths
     // (timing attribution with kernels skipped produces garbage that may end rows early: the
     // early exit is disabled then, so every step still runs)
-    StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, s1_skip ? (1 << 30) : B, 0, 0};
+    StepCtl c{0, alive.empty() ? 0 : alive[0], 0, k, max_cap, s1_skip ? (1 << 30) : B, 0,
+              alive.empty() ? 0 : alive[0]};
     std::memcpy(h_meta, &c, sizeof(StepCtl));
     int* ha = h_meta + 8;
     for (int t = 0; t <= cap_max; ++t) ha[t] = t < max_cap ? alive[t] : 0;
@@ -2249,11 +2254,13 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     explicit PrefetchScope(bool& flag) : f(flag) { f = true; }
     ~PrefetchScope() { f = false; }
   } pscope(cross_prefetch);
+  unrolled_last = false;
   for (int t0 = 0; t0 < max_cap && alive[t0] > 0;) {
     const int bucket = bucket_of(alive[t0]);
     int t1 = t0;
     while (t1 < max_cap && alive[t1] > 0 && bucket_of(alive[t1]) == bucket) ++t1;
     const bool unrolled = BF16 && use_graphs && timed_class == 0 && graph_unroll > 0;
+    unrolled_last = unrolled;
     if (!unrolled || t0 == 0) {
       // loop control (the finished count carries over); the copy also orders every
       // earlier kernel (encoder) before Stage I (cross_prefetch relies on it). The
@@ -2355,6 +2362,9 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
   }
   phase_mark(3);
   phase_valid = true;
+  // rows the Stage-I loop computed (device row counts, unrolled-graph path): statistics
+  const bool row_stat = unrolled_last && host_io && on_device == 0;
+  if (row_stat) CUDA_OK(cudaMemcpyAsync(h_ctl, s_ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, stream));
   if (packed) {
     CUDA_OK(cudaMemcpyAsync(h_out, o_tokens, pk_total, cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaStreamSynchronize(stream));
@@ -2364,6 +2374,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     std::memcpy(out->scores, h_out + pk_scores, (size_t)B * 3 * sizeof(double));
     std::memcpy(out->forced, h_out + pk_forced, B);
     for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+    if (row_stat) stats.stage1_row_steps += h_ctl->pad;
   } else if (host_io) {
     CUDA_OK(cudaMemcpyAsync(out->tokens, o_tokens, (size_t)B * Lmax * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CUDA_OK(cudaMemcpyAsync(out->lens, o_lens, B * sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -2373,6 +2384,7 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
     if (on_device == 0) {  // 2: host buffers, caller synchronises (concurrent engines)
       CUDA_OK(cudaStreamSynchronize(stream));
       for (int i = 0; i < B; ++i) stats.decoder_calls += out->calls[i];
+      if (row_stat) stats.stage1_row_steps += h_ctl->pad;
     }
   }
 }

@@ -1424,7 +1424,7 @@ struct StepCtl {
   int max_cap;   // steps to run at most
   int nrows;     // rows in the batch
   int finished;  // rows finished so far
-  int pad;
+  int pad;       // rows computed so far (plain unrolled graphs)
 };
 
 struct GreedyState {
@@ -1630,16 +1630,39 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
 // Same step advance for the unrolled (plain) loop graphs: the host launches
 // exactly the segment's step count, so no loop condition is set.
 // Once every row (sentence, in beam mode) has finished, R drops to 0 and the
-// remaining captured steps' kernels return immediately.
-__global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive) {
+// remaining captured steps' kernels return immediately. Greedy (done != nullptr):
+// rows finish at their own natural EOS (decoding.py:149-150), so the live count is
+// 1 + the last unfinished row below the cap-predicted one (rows are cap-sorted;
+// every row past it has finished) -- the batch shrinks with the finished tail
+// instead of with the caps. ctl->pad accumulates the rows computed (statistics).
+__global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive, const int* __restrict__ done) {
   pdl_enter();
-  const int t = ctl->t + 1;
-  if (ctl->finished >= ctl->nrows) {
-    ctl->R = 0;
-  } else if (t < ctl->max_cap && alive[t] > 0) {
-    ctl->t = t;
-    ctl->R = alive[t];
-    ctl->pos = t * ctl->k;
+  __shared__ int s_last;
+  const StepCtl c = *ctl;
+  const int t = c.t + 1;
+  const bool more = c.finished < c.nrows && t < c.max_cap && alive[t] > 0;
+  int R = more ? alive[t] : 0;
+  if (done != nullptr && more) {  // (block-uniform branch)
+    if (threadIdx.x == 0) s_last = 0;
+    __syncthreads();
+    int last = 0;
+    for (int r = threadIdx.x; r < R; r += blockDim.x)
+      if (!done[r]) last = r + 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+    if ((threadIdx.x & 31) == 0 && last > 0) atomicMax(&s_last, last);
+    __syncthreads();
+    R = s_last;
+  }
+  if (threadIdx.x == 0) {
+    if (c.finished >= c.nrows) {
+      ctl->R = 0;
+    } else if (more) {
+      ctl->t = t;
+      ctl->R = R;
+      ctl->pos = t * c.k;
+      ctl->pad = c.pad + R;
+    }
   }
 }
 
