@@ -33,7 +33,6 @@ constexpr int DC_THREADS = 256;
 constexpr int DC_D = 512, DC_FF = 2048, DC_H = 8, DC_DH = 64;
 constexpr int DC_RMAX = 4;
 constexpr int DC_CHUNK = 32 * 1024;  // bytes per weight chunk (one ring slot)
-constexpr int DC_NSLOT = 4;
 constexpr int DC_CPL = 14;  // chunks per layer: q k v | wo | qc | woc | w1 x4 | w2 x4
 constexpr int DC_MAXL = 2;  // decoder layers whose biases / LN parameters are staged in shared memory
 constexpr int DC_PRM = 352 + 6 * DC_D;  // floats per layer: own bias slices + six LayerNorm vectors
@@ -60,20 +59,24 @@ struct DcParams {
   int dbg;  // timing attribution only (wrong results): 1 no weight copies, 2 no attention, 4 no broadcasts
 };
 
-// smem layout (bytes)
+// smem layout (bytes) for row bucket RB: the ring takes what the row buffers leave (five
+// 32 KB slots for single-row buckets, four otherwise)
+template <int RB>
 struct DcSmem {
+  static constexpr int NSLOT = RB == 1 ? 5 : 4;
   static constexpr int RING = 0;
-  static constexpr int XS = RING + DC_NSLOT * DC_CHUNK;          // float [R][D]
-  static constexpr int YS = XS + DC_RMAX * DC_D * 4;              // bf16 [R][D]   (LN output, GEMV input)
-  static constexpr int CS = YS + DC_RMAX * DC_D * 2;              // bf16 [R][D]   (attention context)
-  static constexpr int HS = CS + DC_RMAX * DC_D * 2;              // bf16 [R][FF]  (FFN hidden)
-  static constexpr int QS = HS + DC_RMAX * DC_FF * 2;             // float [R][3][64] (this head's q / k / v)
-  static constexpr int PS = QS + DC_RMAX * 3 * 64 * 4;            // float [R][H][2][68] (attention partials)
-  static constexpr int OS = PS + DC_RMAX * DC_H * 2 * 68 * 4;     // float [R][128] GEMV slice staging
-  static constexpr int WS = OS + DC_RMAX * 128 * 4;               // float [8 warps][68] attention merge
-  static constexpr int PRM = WS + 8 * 68 * 4;                     // float [MAXL][DC_PRM] static parameters
+  static constexpr int XS = RING + NSLOT * DC_CHUNK;          // float [R][D]
+  static constexpr int YS = XS + RB * DC_D * 4;              // bf16 [R][D]   (LN output, GEMV input)
+  static constexpr int CS = YS + RB * DC_D * 2;              // bf16 [R][D]   (attention context)
+  static constexpr int HS = CS + RB * DC_D * 2;              // bf16 [R][FF]  (FFN hidden)
+  static constexpr int QS = HS + RB * DC_FF * 2;             // float [R][3][64] (this head's q / k / v)
+  static constexpr int PS = QS + RB * 3 * 64 * 4;            // float [R][H][2][68] (attention partials)
+  static constexpr int OS = PS + RB * DC_H * 2 * 68 * 4;     // float [R][128] GEMV slice staging
+  static constexpr int WS = OS + RB * 128 * 4;               // float [8 warps][68] attention merge
+  static constexpr int PRM = WS + 8 * 68 * 4;                // float [MAXL][DC_PRM] static parameters
   static constexpr int BAR = PRM + DC_MAXL * DC_PRM * 4;
   static constexpr int TOTAL = BAR + 64 + 128;
+  static_assert(TOTAL <= 227 * 1024, "decode cluster shared memory");
 };
 
 __device__ __forceinline__ unsigned long long dc_now() {
@@ -305,18 +308,20 @@ __device__ __forceinline__ void dc_merge_heads(const float* __restrict__ prow /*
 // discarded (their buffers exist), so every loop and shuffle is compile-time uniform
 template <int RB>
 __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) decode_cluster_kernel(DcParams p) {
+  using SM = DcSmem<RB>;
+  constexpr int DC_NSLOT = SM::NSLOT;
   extern __shared__ __align__(1024) uint8_t dsm[];
-  uint8_t* ring = dsm + DcSmem::RING;
-  float* xs = reinterpret_cast<float*>(dsm + DcSmem::XS);
-  bf16* ys = reinterpret_cast<bf16*>(dsm + DcSmem::YS);
-  bf16* cs = reinterpret_cast<bf16*>(dsm + DcSmem::CS);
-  bf16* hs = reinterpret_cast<bf16*>(dsm + DcSmem::HS);
-  float* qs = reinterpret_cast<float*>(dsm + DcSmem::QS);
-  float* ps = reinterpret_cast<float*>(dsm + DcSmem::PS);
-  float* os = reinterpret_cast<float*>(dsm + DcSmem::OS);
-  float* wsb = reinterpret_cast<float*>(dsm + DcSmem::WS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + DcSmem::BAR);  // [DC_NSLOT]
-  float* prm = reinterpret_cast<float*>(dsm + DcSmem::PRM);
+  uint8_t* ring = dsm + SM::RING;
+  float* xs = reinterpret_cast<float*>(dsm + SM::XS);
+  bf16* ys = reinterpret_cast<bf16*>(dsm + SM::YS);
+  bf16* cs = reinterpret_cast<bf16*>(dsm + SM::CS);
+  bf16* hs = reinterpret_cast<bf16*>(dsm + SM::HS);
+  float* qs = reinterpret_cast<float*>(dsm + SM::QS);
+  float* ps = reinterpret_cast<float*>(dsm + SM::PS);
+  float* os = reinterpret_cast<float*>(dsm + SM::OS);
+  float* wsb = reinterpret_cast<float*>(dsm + SM::WS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + SM::BAR);  // [DC_NSLOT]
+  float* prm = reinterpret_cast<float*>(dsm + SM::PRM);
 
   pdl_trigger();
   unsigned long long ts[40];

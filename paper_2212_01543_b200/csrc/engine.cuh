@@ -1684,19 +1684,19 @@ struct Engine : EngineBase {
         ln_fusable(R))
       return false;
     if (cluster_decode_state < 0) {
-      auto prep = [&](auto kern) {
+      auto prep = [&](auto kern, int smem) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DcSmem::TOTAL) != cudaSuccess)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
           return false;
         cudaLaunchConfig_t c = {};
         c.gridDim = dim3(DC_CN);
         c.blockDim = dim3(DC_THREADS);
-        c.dynamicSmemBytes = DcSmem::TOTAL;
+        c.dynamicSmemBytes = smem;
         int n = 0;
         return cudaOccupancyMaxActiveClusters(&n, kern, &c) == cudaSuccess && n >= 1;
       };
-      const bool ok = prep(decode_cluster_kernel<1>) && prep(decode_cluster_kernel<2>) &&
-                      prep(decode_cluster_kernel<4>);
+      const bool ok = prep(decode_cluster_kernel<1>, DcSmem<1>::TOTAL) &&
+                      prep(decode_cluster_kernel<2>, DcSmem<2>::TOTAL) && prep(decode_cluster_kernel<4>, DcSmem<4>::TOTAL);
       cudaGetLastError();
       cluster_decode_state = ok ? 1 : 0;
     }
@@ -1730,11 +1730,11 @@ struct Engine : EngineBase {
     Scope sc(this, K_GEMM | K_ATTN, 2.0 * Ld * (6.0 * d * d + 2.0 * d * ff), 2.0 * R * Ld * (6.0 * d * d + 2.0 * d * ff));
     const int Rp = path_rows > 0 ? path_rows : R;
     if (Rp <= 1)
-      launch(decode_cluster_kernel<1>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+      launch(decode_cluster_kernel<1>, DC_CN, DC_THREADS, DcSmem<1>::TOTAL, dp);
     else if (Rp <= 2)
-      launch(decode_cluster_kernel<2>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+      launch(decode_cluster_kernel<2>, DC_CN, DC_THREADS, DcSmem<2>::TOTAL, dp);
     else
-      launch(decode_cluster_kernel<4>, DC_CN, DC_THREADS, DcSmem::TOTAL, dp);
+      launch(decode_cluster_kernel<4>, DC_CN, DC_THREADS, DcSmem<4>::TOTAL, dp);
     check_launch();
   }
 
@@ -1807,7 +1807,8 @@ struct Engine : EngineBase {
     try {
       for (int u = 0; u < U; ++u) {
         stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
-        launch(stage1_advance_plain_kernel, 1, 256, 0, s_ctl, s_alive, beam == 1 ? (const int*)s_done : nullptr);
+        launch(stage1_advance_plain_kernel, 1, bucket <= 32 ? 32 : 256, 0, s_ctl, s_alive,
+               beam == 1 ? (const int*)s_done : nullptr);
         check_launch();
       }
     } catch (...) {

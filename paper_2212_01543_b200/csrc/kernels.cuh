@@ -1643,16 +1643,19 @@ __global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict_
   const bool more = c.finished < c.nrows && t < c.max_cap && alive[t] > 0;
   int R = more ? alive[t] : 0;
   if (done != nullptr && more) {  // (block-uniform branch)
-    if (threadIdx.x == 0) s_last = 0;
-    __syncthreads();
     int last = 0;
     for (int r = threadIdx.x; r < R; r += blockDim.x)
       if (!done[r]) last = r + 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-    if ((threadIdx.x & 31) == 0 && last > 0) atomicMax(&s_last, last);
-    __syncthreads();
-    R = s_last;
+    if (blockDim.x > 32) {  // small buckets launch one warp: no block barrier on the step's critical path
+      if (threadIdx.x == 0) s_last = 0;
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0 && last > 0) atomicMax(&s_last, last);
+      __syncthreads();
+      last = s_last;
+    }
+    R = last;
   }
   if (threadIdx.x == 0) {
     if (c.finished >= c.nrows) {
