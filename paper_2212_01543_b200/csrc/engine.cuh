@@ -1170,7 +1170,7 @@ struct Engine : EngineBase {
                    const int* M_dev = nullptr, const float* ln_g = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
-      if (kt == 1 && gemv_vocab_ok(R)) {
+      if ((kt == 1 || (kt <= 5 && !ln_g)) && gemv_vocab_ok(R)) {
         parts.ntiles = cdiv(V, GV_VTILE);
         Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
         const bf16* yb = reinterpret_cast<const bf16*>(y);
@@ -1179,7 +1179,9 @@ struct Engine : EngineBase {
         const int grid = cdiv(V, GV_VTILE);
 #define HRT_GVV(NT)                                                                                          \
   do {                                                                                                       \
-    if (ln_g)                                                                                                \
+    if (kt > 1)                                                                                              \
+      launch(gemv_vocab_kernel<NT, false, 5>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
+    else if (ln_g)                                                                                           \
       launch(gemv_vocab_kernel<NT, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
     else                                                                                                     \
       launch(gemv_vocab_kernel<NT, false>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \

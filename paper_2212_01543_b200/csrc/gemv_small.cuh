@@ -383,14 +383,17 @@ struct GvStat {
 constexpr int GV_VWARPS = 8;
 constexpr int GV_VTILE = GV_VWARPS * 16;
 
-// Vocabulary statistics for M <= 8 * NT rows (KT = 1: greedy selection and
-// the Stage-II argmax): parts.ntiles must be cdiv(V, GV_VTILE).
-template <int NT, bool LNA = false>
+// Vocabulary statistics for M <= 8 * NT rows: parts.ntiles must be cdiv(V, GV_VTILE).
+// KT = 1: {max, sum, top-1} (greedy selection, Stage-II argmax); KT > 1 (beam search,
+// decoding.py:113 top-(b+1)): the tile's KT best allowed (value desc, id asc) per row,
+// picked by one thread per row from the 128 logits staged in shared memory.
+template <int NT, bool LNA = false, int KT = 1>
 __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ E, int V, int K, int M,
                                                                 const int* __restrict__ M_dev, VocabParts parts,
                                                                 int norm_allowed, GvLN ln) {
   __shared__ float4 ws[GV_VWARPS][8 * NT];
+  __shared__ float lg[KT > 1 ? 8 * NT : 1][KT > 1 ? GV_VTILE : 1];  // KT > 1: the tile's logits per row
   __shared__ float2 lnst[LNA ? 8 * NT : 1];
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
@@ -465,6 +468,10 @@ __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* 
       if (has && f1 < V) s.add(c[j][2 + e], f1, norm_allowed);
       const int row = 8 * j + 2 * t4 + e;
       if (f0 == EOS_ID && row < M) parts.eos[row] = c[j][e];
+      if constexpr (KT > 1) {
+        lg[row][warp * 16 + g] = c[j][e];
+        lg[row][warp * 16 + g + 8] = c[j][2 + e];
+      }
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) {
         const float om = __shfl_xor_sync(0xffffffffu, s.mx, o);
@@ -488,8 +495,41 @@ __global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* 
     const size_t o = (size_t)r * parts.ntiles + blockIdx.x;
     parts.mx[o] = s.mx;
     parts.sum[o] = s.sum;
-    parts.val[o] = s.bv;
-    parts.id[o] = s.bi;
+    if constexpr (KT == 1) {
+      parts.val[o] = s.bv;
+      parts.id[o] = s.bi;
+    } else {
+      float tv[KT];
+      int ti[KT];
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        tv[i] = -INFINITY;
+        ti[i] = 0x7fffffff;
+      }
+      const int c0 = blockIdx.x * GV_VTILE;
+      for (int q = 0; q < GV_VTILE; ++q) {
+        const int id = c0 + q;
+        if (id >= V || !id_allowed(id)) continue;
+        float v = lg[r][q];
+        int vi = id;
+        if (!better(v, vi, tv[KT - 1], ti[KT - 1])) continue;
+#pragma unroll
+        for (int i = 0; i < KT; ++i)  // insertion into the sorted list
+          if (better(v, vi, tv[i], ti[i])) {
+            const float sv = tv[i];
+            const int si = ti[i];
+            tv[i] = v;
+            ti[i] = vi;
+            v = sv;
+            vi = si;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        parts.val[o * KT + i] = tv[i];
+        parts.id[o * KT + i] = ti[i];
+      }
+    }
   }
 }
 

@@ -1369,41 +1369,100 @@ __device__ __forceinline__ RowStat merge_row(const VocabParts& parts, int row, i
   rs.lse = logf(s);
   rs.eos = parts.eos[row];
   rs.kt = kt;
-  // kt <= KT rounds; in round r every lane scans its tiles' sorted lists for
-  // the best entry strictly worse than the previous round's winner.
-  float pv = INFINITY;
-  int pid = -1;
-  for (int r = 0; r < kt; ++r) {
-    float bv = -INFINITY;
-    int bid = 0x7fffffff;
-    for (int t = lane; t < parts.ntiles; t += 32) {
-      for (int i = 0; i < KT; ++i) {
-        const float v = parts.val[(base + t) * KT + i];
-        const int id = parts.id[(base + t) * KT + i];
-        if (id == 0x7fffffff) break;
-        if (better(pv, pid, v, id) && better(v, id, bv, bid)) {
-          bv = v;
-          bid = id;
-          break;  // lists are sorted: first entry worse than the previous winner is this tile's best
+  // kt <= KT rounds of a k-way merge: every lane holds a cursor into each of its
+  // (<= 8) tiles' sorted top-KT lists and that tile's current head in registers; a
+  // round takes the warp-best head (lowest id on ties), and only the owning lane
+  // advances that tile's cursor (one load) -- no list is rescanned.
+  constexpr int MAXP = 8;
+  if (parts.ntiles > 32 * MAXP) {  // (not reached for V <= 32768: at most 256 tiles per row)
+    float pv = INFINITY;
+    int pid = -1;
+    for (int r = 0; r < kt; ++r) {
+      float bv = -INFINITY;
+      int bid = 0x7fffffff;
+      for (int t = lane; t < parts.ntiles; t += 32) {
+        for (int i = 0; i < KT; ++i) {
+          const float v = parts.val[(base + t) * KT + i];
+          const int id = parts.id[(base + t) * KT + i];
+          if (id == 0x7fffffff) break;
+          if (better(pv, pid, v, id) && better(v, id, bv, bid)) {
+            bv = v;
+            bid = id;
+            break;
+          }
         }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+        if (better(ov, oid, bv, bid)) {
+          bv = ov;
+          bid = oid;
+        }
+      }
+      rs.val[r] = bv;
+      rs.id[r] = bid;
+      pv = bv;
+      pid = bid;
     }
+    return rs;
+  }
+  float hv[MAXP];
+  int hid[MAXP], cur[MAXP];
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) {
+    const int t = lane + 32 * i;
+    cur[i] = 0;
+    hv[i] = -INFINITY;
+    hid[i] = 0x7fffffff;
+    if (t < parts.ntiles) {
+      hv[i] = parts.val[(base + t) * KT];
+      hid[i] = parts.id[(base + t) * KT];
+    }
+  }
+  for (int r = 0; r < kt; ++r) {
+    float bv = -INFINITY;
+    int bid = 0x7fffffff, bslot = -1;
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i)
+      if (hid[i] != 0x7fffffff && better(hv[i], hid[i], bv, bid)) {
+        bv = hv[i];
+        bid = hid[i];
+        bslot = i;
+      }
+    float wv = bv;
+    int wid = bid;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
-      if (better(ov, oid, bv, bid)) {
-        bv = ov;
-        bid = oid;
+      const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int oid = __shfl_xor_sync(0xffffffffu, wid, o);
+      if (better(ov, oid, wv, wid)) {
+        wv = ov;
+        wid = oid;
       }
     }
-    rs.val[r] = bv;
-    rs.id[r] = bid;
-    pv = bv;
-    pid = bid;
+    rs.val[r] = wv;
+    rs.id[r] = wid;
+    if (wid == 0x7fffffff) continue;  // fewer generable candidates than kt (caller handles)
+    // the owner of the winning head advances that tile's cursor (ids are unique across tiles)
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i)
+      if (i == bslot && bid == wid) {
+        const int t = lane + 32 * i;
+        cur[i] += 1;
+        if (cur[i] < KT) {
+          hv[i] = parts.val[(base + t) * KT + cur[i]];
+          hid[i] = parts.id[(base + t) * KT + cur[i]];
+        } else {
+          hv[i] = -INFINITY;
+          hid[i] = 0x7fffffff;
+        }
+      }
   }
   return rs;
 }
+
 
 // ---------------------------------------------------------------------------
 // Stage-I greedy selection (decoding.py:102-150 with beam = 1): one warp per
