@@ -149,6 +149,10 @@ hrt_status hrt_at_translate_batch(hrt_engine* eng, const int32_t* ids, const int
  *   "graph_unroll"  steps per captured graph (power of two <= 32, default 16); 0: one conditional
  *                   WHILE-node graph per row bucket (the original design, measured slower)
  *   "cluster"       1 (default): large-M tcgen05 GEMMs as CTA pairs sharing the weight tile
+ *   "ln_row"        1 (default, d = 512, bf16): residual projection + following LayerNorm in one
+ *                   launch (cta_group::2 CTA pairs, whole 512-column rows per CTA, TMA-staged
+ *                   epilogue); 0: GEMM + LayerNorm kernel; 2 / 3: register-epilogue variants
+ *   "res_red"       1 (default): residual GEMM epilogues as L2 reductions (same bits)
  *   "gemv", "gemv_max_m", "bn32", "attn_heads", "attn_rows", "splitk", "ln_fuse", "tail_ln",
  *   "l2_persist": kernel-path switches documented in DESIGN.md §4 / §7. */
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);

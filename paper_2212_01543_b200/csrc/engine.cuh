@@ -17,6 +17,7 @@
 #include <memory>
 #include <numeric>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -29,6 +30,7 @@
 #include "kernels.cuh"
 #include "tc_gemm.cuh"
 #include "tc_gemm_ln.cuh"
+#include "tc_gemm_lnrow.cuh"
 #include "decode_cluster.cuh"
 #include "tmap.h"
 
@@ -729,6 +731,18 @@ struct Engine : EngineBase {
       const CUtensorMap& tc = tmap_out<Epi>(epi, a_cap, N, ta);
       SplitK sk{1, sk_ws, sk_counters};
       if constexpr (!Epi::kRowWise && CL == 1) sk.splits = choose_splits(M, N, K, BN);
+      if constexpr (std::is_same<Epi, EpiResidual>::value) {
+        if (res_red && sk.splits == 1) {
+          Epi e2 = epi;
+          e2.red = true;
+          const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL);
+          const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
+          launch_cluster = CL;
+          launch(kern, grid, TC_THREADS, smem, ta, tb, tc, M, N, K, M_dev, e2, sk);
+          launch_cluster = 1;
+          return;
+        }
+      }
       // M: count, or upper bound with M_dev; CL = 2 works on vertical tile pairs
       const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL) * sk.splits;
       const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
@@ -872,11 +886,43 @@ struct Engine : EngineBase {
   }
   // residual + LayerNorm in the tcgen05 epilogue (tc_gemm_ln.cuh): rows above the GEMV
   // regime, d a multiple of 256 with d / 256 in {1, 2, 4} (a cluster of d / 256 CTAs per row block)
+  // residual GEMM epilogues (tcgen05, no split-K) as L2 reductions: option "res_red"
+  bool res_red = true;
   bool use_ln_epi = false;  // option "ln_epi" (correct, measured slower than GEMM + LN kernel: off)
   bool ln_epi_ok(int M, int K) const {
     const int nc = d / TL_BN;
     return BF16 && use_ln_epi && !gemv_ok(M, K) && d % TL_BN == 0 && (nc == 1 || nc == 2 || nc == 4) &&
            K % TC_BK == 0;
+  }
+  // full-row form (tc_gemm_lnrow.cuh, d = 512): option "ln_row" = 1 TMA-staged lane-per-row
+  // epilogue with the updated rows kept in TMEM, 2 / 3 register epilogue re-reading them from
+  // L2 (accumulator released after pass 1) / keeping them in TMEM; used
+  // from ln_row_min_tiles 128-row blocks up (Stage-I buckets keep the narrow-tile GEMM + LN)
+  int ln_row = 1;
+  int ln_row_min_tiles = 16;
+  bool ln_row_ok(int M, int K) const {
+    return BF16 && ln_row != 0 && d == LR_D && K % TC_BK == 0 && cdiv(M, TC_BM) >= ln_row_min_tiles &&
+           !gemv_ok(M, K);
+  }
+  std::map<std::tuple<const void*, int>, CUtensorMap> tmaps_x;
+  template <int MODE>
+  void lnrow_launch(const T* A, int a_cap, int lda, int M, const T* W, int K, const ResLnArgs& ra,
+                    const int* M_dev) {
+    if constexpr (BF16) {
+      constexpr int ST = 3;  // 3 x 48 KB ring + 32 KB transpose buffers + row statistics
+      auto kern = tc_gemm_resln_row_kernel<ST, MODE>;
+      const int smem = LrSmem<ST>::TOTAL;
+      smem_optin(kern, smem);
+      const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
+      const CUtensorMap& tb = tmap(W, d, K, K, LR_D / 4);
+      auto key = std::make_tuple(static_cast<const void*>(ra.x), M);
+      auto itx = tmaps_x.find(key);
+      if (itx == tmaps_x.end()) itx = tmaps_x.emplace(key, make_tmap_f32_tile(ra.x, M, d, ra.ldx)).first;
+      const int grid = std::min(cdiv(cdiv(M, TC_BM), 2), resident_clusters(kern, smem, 2)) * 2;
+      launch_cluster = 2;
+      launch(kern, grid, TC_THREADS, smem, ta, tb, itx->second, M, K, M_dev, ra);
+      launch_cluster = 1;
+    }
   }
   template <int NC>
   void resln_launch(const T* A, int a_cap, int lda, int M, const T* W, int K, const ResLnArgs& ra,
@@ -896,9 +942,26 @@ struct Engine : EngineBase {
   }
   // x += A W^T + bias, then y = LN(x) (rows out_row[r] of y when given): one fused
   // launch on the tcgen05 path, GEMV tail-LN or GEMM + LN kernel otherwise
+  // "<current tag><suffix>" (timing attribution of a call site's trailing launch)
+  std::map<std::pair<const char*, const char*>, std::string> sub_tags;
+  const char* sub_tag(const char* suffix) {
+    if (cur_tag == nullptr) return nullptr;
+    std::string& t = sub_tags[{cur_tag, suffix}];
+    if (t.empty()) t = std::string(cur_tag) + suffix;
+    return t.c_str();
+  }
   void gemm_res_ln(const T* A, int a_cap, int lda, int M, const T* W, int K, float* x, const float* bias,
                    const float* g, const float* b, T* y, const int* M_dev, const int* out_row = nullptr) {
     if (M <= 0) return;
+    if (ln_row_ok(M, K)) {
+      Scope sc(this, K_GEMM, (double)sizeof(T) * ((double)d * K + (double)M * K), 2.0 * M * d * K);
+      const ResLnArgs ra{x, d, bias, g, b, reinterpret_cast<bf16*>(y), d, out_row};
+      if (ln_row == 2) lnrow_launch<0>(A, a_cap, lda, M, W, K, ra, M_dev);
+      else if (ln_row == 3) lnrow_launch<1>(A, a_cap, lda, M, W, K, ra, M_dev);
+      else lnrow_launch<2>(A, a_cap, lda, M, W, K, ra, M_dev);
+      check_launch();
+      return;
+    }
     if (ln_epi_ok(M, K)) {
       Scope sc(this, K_GEMM, (double)sizeof(T) * ((double)d * K + (double)M * K), 2.0 * M * d * K);
       const ResLnArgs ra{x, d, bias, g, b, reinterpret_cast<bf16*>(y), d, out_row};
@@ -917,6 +980,7 @@ struct Engine : EngineBase {
       return;
     }
     gemm(K_GEMM, A, a_cap, lda, M, W, d, K, EpiResidual{x, d, bias}, M_dev);
+    Tag _t(this, sub_tag(".ln"));
     layernorm(x, M, g, b, y, out_row, nullptr, M_dev);
   }
   // LayerNorm feeding a projection: fused into the GEMV prologue on the
@@ -1913,6 +1977,12 @@ struct Engine : EngineBase {
     } else if (name == "cluster_decode") {
       cluster_decode_mode = value;
       drop_loop_graphs();
+    } else if (name == "ln_row") {
+      ln_row = value;
+    } else if (name == "ln_row_min_tiles") {
+      ln_row_min_tiles = value;
+    } else if (name == "res_red") {
+      res_red = value != 0;
     } else if (name == "ln_epi") {
       use_ln_epi = value != 0;
       drop_loop_graphs();

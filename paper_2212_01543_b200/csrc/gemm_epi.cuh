@@ -117,6 +117,10 @@ struct EpiResidual {
   float* x;
   int ldx;
   const float* bias;
+  // tcgen05 epilogue only: x += acc + bias as fire-and-forget L2 reductions
+  // (red.global.add.v4.f32) instead of a prefetched read-modify-write. One add per
+  // element, so the result is the same bits as the load / add / store form.
+  bool red = false;
   __host__ __device__ int ld() const { return ldx; }
   __device__ __forceinline__ void apply4(int row, int col, float4 v) const {
     float* p = x + (size_t)row * ldx + col;
@@ -150,6 +154,7 @@ struct EpiResidual {
   // requested one chunk ahead, so their DRAM latency overlaps the previous chunk
   static constexpr bool kPrefetch = true;
   __device__ __forceinline__ void prefetch8(int row0, int col, int M, float4 (&p)[8]) const {
+    if (red) return;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       p[i] = row0 + 4 * i < M ? *reinterpret_cast<const float4*>(x + (size_t)(row0 + 4 * i) * ldx + col)
@@ -157,6 +162,15 @@ struct EpiResidual {
   }
   __device__ __forceinline__ void apply8_pre(int row0, int col, const float4* v, int M, const float4 (&prev)[8]) const {
     const float4 b = *reinterpret_cast<const float4*>(bias + col);
+    if (red) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (row0 + 4 * i < M)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(x + (size_t)(row0 + 4 * i) * ldx + col),
+                       "f"(v[i].x + b.x), "f"(v[i].y + b.y), "f"(v[i].z + b.z), "f"(v[i].w + b.w)
+                       : "memory");
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (row0 + 4 * i < M) {

@@ -55,4 +55,20 @@ inline CUtensorMap make_tmap_bf16_store(const void* base, uint64_t rows, uint64_
   return m;
 }
 
+// fp32 [rows, cols] (row stride `ld` elements) in 32 x 32 boxes (128-byte rows, 128-byte
+// swizzle): residual-stream chunks loaded and stored by the LayerNorm epilogue
+inline CUtensorMap make_tmap_f32_tile(const void* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (f32 tile) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 }  // namespace hrt

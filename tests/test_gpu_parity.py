@@ -584,11 +584,18 @@ def test_bf16_c2_shape_large_batch(hrt):
     # residual + LayerNorm fused into the tcgen05 epilogue (cluster of d / 256 CTAs exchanging
     # row statistics over DSMEM): only the LN summation order differs from GEMM + LN kernel
     eng.set_option("cluster", 1)
+    eng.set_option("ln_row", 0)
     eng.set_option("ln_epi", 1)
     e = eng.translate_batch(srcs, 2, max_steps=caps)
     eng.set_option("ln_epi", 0)
     same = sum(p == q for x, y in zip(a, e) for p, q in zip(x.tokens, y.tokens))
     assert same / sum(max(len(x.tokens), len(y.tokens)) for x, y in zip(a, e)) > 0.98
+    # the default full-row residual + LayerNorm epilogue (ln_row = 1, one CTA per 128-row block
+    # holding all 512 columns) against GEMM + LN kernel: again only the LN summation order differs
+    u = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("ln_row", 1)
+    same = sum(p == q for x, y in zip(a, u) for p, q in zip(x.tokens, y.tokens))
+    assert same / sum(max(len(x.tokens), len(y.tokens)) for x, y in zip(a, u)) > 0.98
     f32 = hrt.Engine(model, dtype="float32", max_sentences=len(srcs), max_beam=1)
     c = f32.translate_batch(srcs, 2, max_steps=caps)
     agree = total = 0

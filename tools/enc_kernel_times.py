@@ -10,6 +10,9 @@ eng = hrt.Engine(hrt.HRTModel.random(spec["shape"], spec["seed"]), dtype="bfloat
 srcs = W.make_sources(B, 1001, spec["lengths"])
 caps = W.stage1_caps(srcs, 2)
 ids = np.concatenate([np.asarray(s, np.int32) for s in srcs]); lens = [len(s) for s in srcs]
+for kv in filter(None, os.environ.get("OPTS", "").split(",")):
+    k, v = kv.split("=")
+    eng.set_option(k, int(v))
 for _ in range(2):
     eng.translate_arrays(ids, lens, k=2, max_steps=caps)
 eng.timing_enable("all", True)
