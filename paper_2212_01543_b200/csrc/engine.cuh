@@ -905,13 +905,13 @@ struct Engine : EngineBase {
            !gemv_ok(M, K);
   }
   std::map<std::tuple<const void*, int>, CUtensorMap> tmaps_x;
-  template <int MODE>
+  template <int MODE, int ST = 3>
   void lnrow_launch(const T* A, int a_cap, int lda, int M, const T* W, int K, const ResLnArgs& ra,
                     const int* M_dev) {
     if constexpr (BF16) {
-      constexpr int ST = 3;  // 3 x 48 KB ring + 32 KB transpose buffers + row statistics
+      // ST x 48 KB operand ring (+ 32 KB per-warp buffers unless MODE 2 borrows 4 stages) + statistics
       auto kern = tc_gemm_resln_row_kernel<ST, MODE>;
-      const int smem = LrSmem<ST>::TOTAL;
+      const int smem = LrSmem<ST, lr_stg<ST, MODE>()>::TOTAL;
       smem_optin(kern, smem);
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, d, K, K, LR_D / 4);
@@ -958,6 +958,7 @@ struct Engine : EngineBase {
       const ResLnArgs ra{x, d, bias, g, b, reinterpret_cast<bf16*>(y), d, out_row};
       if (ln_row == 2) lnrow_launch<0>(A, a_cap, lda, M, W, K, ra, M_dev);
       else if (ln_row == 3) lnrow_launch<1>(A, a_cap, lda, M, W, K, ra, M_dev);
+      else if (ln_row == 4) lnrow_launch<2, 4>(A, a_cap, lda, M, W, K, ra, M_dev);
       else lnrow_launch<2>(A, a_cap, lda, M, W, K, ra, M_dev);
       check_launch();
       return;

@@ -40,30 +40,43 @@
 namespace hrt {
 
 constexpr int LR_D = 512;
-constexpr int LR_SLOTS = 5;  // MODE 2: residual chunk buffers per epilogue warp (1 transpose buffer + 4 ring)
+constexpr int LR_SLOTS_MAX = 6;
 
-template <int STAGES>
+// STG: per-warp 32 x 32 fp32 buffers outside the operand ring (the register epilogues'
+// transpose buffers; MODE 2 with a 3-stage ring: each warp's first residual slot)
+template <int STAGES, bool STG>
 struct LrSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;          // 16 KB: this CTA's 128 rows
   static constexpr int BQ_BYTES = (LR_D / 4) * TC_BK * 2;    // 16 KB: 128 weight rows per N = 256 half
   static constexpr int STAGE_BYTES = A_BYTES + 2 * BQ_BYTES;  // 48 KB
-  static constexpr int STG_OFFSET = STAGES * STAGE_BYTES;    // per-warp 32 x 32 fp32 transpose buffers
-  static constexpr int STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
+  static constexpr int STG_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int STG_BYTES = STG ? TC_EPI_WARPS * 32 * TC_STG_LD * 4 : 0;
   static constexpr int ST_OFFSET = STG_OFFSET + STG_BYTES;   // row statistics [2 parity][2 halves][128] float2
   static constexpr int ST_BYTES = 2 * 2 * TC_BM * 8;
   static constexpr int PRM_OFFSET = ST_OFFSET + ST_BYTES;  // bias, LN gain, LN bias [3][512] fp32
   static constexpr int PRM_BYTES = 3 * LR_D * 4;
   static constexpr int BAR_OFFSET = PRM_OFFSET + PRM_BYTES;
   static constexpr int TOTAL = BAR_OFFSET + 512 + 1024;
+  // MODE 2 residual slots per epilogue warp: 4 KB slices of the ring (+ the STG buffer)
+  static constexpr int RING_SLOTS = (STAGES * STAGE_BYTES / (4096 * TC_EPI_WARPS)) < (STG ? LR_SLOTS_MAX - 1 : LR_SLOTS_MAX)
+                                        ? STAGES * STAGE_BYTES / (4096 * TC_EPI_WARPS)
+                                        : (STG ? LR_SLOTS_MAX - 1 : LR_SLOTS_MAX);
+  static constexpr int SLOTS = RING_SLOTS + (STG ? 1 : 0);
 };
+template <int STAGES, int MODE>
+__host__ __device__ constexpr bool lr_stg() {
+  return MODE != 2 || STAGES < 4;
+}
 
 template <int STAGES, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_resln_row_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmX, int M, int K, const int* __restrict__ M_dev,
                              ResLnArgs ep) {
-  using L = LrSmem<STAGES>;
+  constexpr bool USE_STG = lr_stg<STAGES, MODE>();
+  using L = LrSmem<STAGES, USE_STG>;
   constexpr bool KEEP = MODE != 0;
+  constexpr int NSL = L::SLOTS;
   constexpr int CL = 2;
   constexpr int HB = LR_D / 2;  // columns per MMA instruction (N = 256)
   constexpr int QB = LR_D / 4;  // weight rows per CTA per N half
@@ -76,7 +89,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tempty = tfull + 1;  // leader's: both CTAs' epilogue warps
   uint64_t* ring_free = tempty + 1;  // MODE 2: the epilogue gave the operand ring back
   uint64_t* xbar = ring_free + 1;    // MODE 2: [8 warps][5 slots] residual chunk arrivals
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + TC_EPI_WARPS * LR_SLOTS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + TC_EPI_WARPS * LR_SLOTS_MAX);
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5;
@@ -97,7 +110,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_init(tfull, 1);
     mbar_init(tempty, CL * TC_EPI_WARPS);
     mbar_init(ring_free, TC_EPI_WARPS);
-    for (int j = 0; j < TC_EPI_WARPS * LR_SLOTS; ++j) mbar_init(&xbar[j], 1);
+    for (int j = 0; j < TC_EPI_WARPS * LR_SLOTS_MAX; ++j) mbar_init(&xbar[j], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
@@ -210,16 +223,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int half = ew >> 2;
     const int cbeg = half * HB;
     constexpr int NCH = HB / 32;  // chunks per warp per pass
-    uint8_t* slot0 = smem + L::STG_OFFSET + ew * 4096;
-    uint8_t* ring = smem + ew * (4 * 4096);
-    auto slot_ptr = [&](int sl) { return sl == 0 ? slot0 : ring + (sl - 1) * 4096; };
-    uint64_t* xb = xbar + ew * LR_SLOTS;
+    // slot 0 is the warp's STG buffer when the ring leaves room for one (it can be filled
+    // while the MMAs still use the ring: the next unit's first chunk is requested early)
+    uint8_t* ring = smem + ew * (L::RING_SLOTS * 4096);
+    auto slot_ptr = [&](int sl) {
+      if constexpr (USE_STG) return sl == 0 ? smem + L::STG_OFFSET + ew * 4096 : ring + (sl - 1) * 4096;
+      else return ring + sl * 4096;
+    };
+    uint64_t* xb = xbar + ew * LR_SLOTS_MAX;
     uint32_t ph = 0;  // per-slot phase bits
     auto load_chunk = [&](int sl, int c, int rblk) {  // lane 0
       mbar_arrive_expect_tx(&xb[sl], 4096);
       tma_load_2d(slot_ptr(sl), &tmX, &xb[sl], c, rblk);
     };
-    if (cid < num_units && lane == 0) load_chunk(0, cbeg, (cid * CL + crank) * TC_BM + quarter * 32);
+    if (USE_STG && cid < num_units && lane == 0) load_chunk(0, cbeg, (cid * CL + crank) * TC_BM + quarter * 32);
     int it = 0;
     for (int u = cid; u < num_units; u += ncl, ++it) {
       const int rblk = (u * CL + crank) * TC_BM + quarter * 32;  // this warp's 32-row block
@@ -229,14 +246,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       // the operand ring is idle now: chunks 1..3 go straight in
       if (lane == 0)
-        for (int j = 1; j < 4; ++j) load_chunk(j, cbeg + 32 * j, rblk);
+        for (int j = USE_STG ? 1 : 0; j < NSL - 1 && j < NCH; ++j) load_chunk(j, cbeg + 32 * j, rblk);
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
       // ---- pass 1: x += acc + bias (TMA in / out), row statistics, x kept in TMEM ----
       float cnt = 0.f, rmean = 0.f, rm2 = 0.f;
 #pragma unroll 1
       for (int j = 0; j < NCH; ++j) {
         const int c = cbeg + 32 * j;
-        const int sl = j % LR_SLOTS;
+        const int sl = j % NSL;
         float v[32];
         tmem_ld32(tbase + c, v);
         mbar_wait(&xb[sl], (ph >> sl) & 1);
@@ -285,10 +302,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) q += (v[i] - bm) * (v[i] - bm);
         chan_merge(cnt, rmean, rm2, 32.f, bm, q);
-        // the slot of chunk j - 1 is refilled with chunk j + 4 once its store has read it
-        if (lane == 0 && j + 4 < NCH) {
+        // the slot of chunk j - 1 is refilled with chunk j + NSL - 1 once its store has read it
+        if (lane == 0 && j + NSL - 1 < NCH) {
           bulk_wait_read<1>();
-          load_chunk((j + 4) % LR_SLOTS, c + 128, rblk);
+          load_chunk((j + NSL - 1) % NSL, c + 32 * (NSL - 1), rblk);
         }
         __syncwarp();
       }
@@ -297,7 +314,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (lane == 0) {
         bulk_wait_read<0>();
         mbar_arrive(ring_free);
-        if (u + ncl < num_units) load_chunk(0, cbeg, ((u + ncl) * CL + crank) * TC_BM + quarter * 32);
+        if (USE_STG && u + ncl < num_units) load_chunk(0, cbeg, ((u + ncl) * CL + crank) * TC_BM + quarter * 32);
       }
       tmem_st_wait();
       // ---- exchange the two column halves' row partials ----

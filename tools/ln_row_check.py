@@ -24,7 +24,7 @@ ref = f32.translate_batch(srcs, 2, max_steps=caps)
 del f32
 eng = hrt.Engine(model, dtype="bfloat16", max_sentences=B, max_beam=1)
 outs = {}
-for v in (0, 1, 2, 3, 0):
+for v in (0, 1, 2, 3, 4, 0):
     eng.set_option("ln_row", v)
     outs[v] = eng.translate_batch(srcs, 2, max_steps=caps)
     print(f"ln_row={v}: vs fp32 {agree(outs[v], ref):.4f}  vs unfused bf16 {agree(outs[v], outs[0]):.4f}", flush=True)
