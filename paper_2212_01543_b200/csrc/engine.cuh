@@ -103,6 +103,7 @@ struct Engine : EngineBase {
   };
   std::map<int, LoopGraph> loop_graphs;
   bool use_graphs = true;
+  int attn_head_groups = 4;  // option "attn_head_groups": CTAs per (sequence, query block) in that kernel
   int attn_heads_mode = 1;  // option "attn_heads": all-heads-per-CTA prefill attention (0 off, 1 auto, 2 always)
   int attn_rows_mode = 1;  // option "attn_rows": CTA-per-row decode attention (0 off, 1 >= 256 rows, 2 always)
   // set in the fused Stage-I loop only: the encoder is complete (a stream copy separates
@@ -799,11 +800,12 @@ struct Engine : EngineBase {
   // widest N tile that still fills ~0.6 of the SMs (large-M encoder / Stage-II
   // GEMMs -> 256, Stage-I GEMMs with few row tiles -> 128 or 64)
   int bn32_mode = 1;  // option "bn32": 32-column tiles when 64-column tiles leave most SMs idle
+  int fill_pct = 60;  // option "fill": SM share the widest tile must still reach
   int choose_bn(int M, int N) const {
     const int mt = cdiv(M, TC_BM);
     if (M > 128)
       for (int bn : {256, 128})
-        if (mt * cdiv(N, bn) * 10 >= num_sms * 6) return bn;
+        if (mt * cdiv(N, bn) * 100 >= num_sms * fill_pct) return bn;
     if (bn32_mode && mt * cdiv(N, 64) * 2 < num_sms) return 32;
     return 64;
   }
@@ -1122,17 +1124,20 @@ struct Engine : EngineBase {
       // all heads per CTA (K/V rows fetched once); with few work items per-head CTAs spread wider
       if (dh == 64 && (H == 1 || H == 2 || H == 4 || H == 8) &&
           (attn_heads_mode == 2 || (attn_heads_mode == 1 && n_items >= num_sms))) {
-        const size_t smem = attn_heads_smem(d);
+        // heads per CTA: all (K / V rows fetched once), or H / attn_head_groups (smaller CTAs,
+        // more of them resident per SM)
+        const int ht = std::max(1, H / std::max(1, attn_head_groups));
+        const size_t smem = attn_heads_smem(ht * dh);
         auto go = [&](auto kern) {
           smem_optin(kern, smem);
-          launch(kern, dim3(n_items), 2 * H * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len, kv_map,
-                 kv_off, kv_len, key_ok, causal, att_scale, H);
+          launch(kern, dim3(n_items, H / ht), 2 * ht * 32, smem, it2, q, qs, k, v, kvs, out, os, q_off, q_slot, q_len,
+                 kv_map, kv_off, kv_len, key_ok, causal, att_scale, H);
         };
-        if (H == 8)
+        if (ht == 8)
           go(attn_prefill_heads_kernel<8>);
-        else if (H == 4)
+        else if (ht == 4)
           go(attn_prefill_heads_kernel<4>);
-        else if (H == 2)
+        else if (ht == 2)
           go(attn_prefill_heads_kernel<2>);
         else
           go(attn_prefill_heads_kernel<1>);
@@ -1939,6 +1944,10 @@ struct Engine : EngineBase {
     else if (name == "tail_ln") {
       use_tail_ln = value != 0;
       drop_loop_graphs();
+    } else if (name == "attn_head_groups") {
+      attn_head_groups = std::max(1, value);
+    } else if (name == "fill") {
+      fill_pct = std::max(1, std::min(100, value));
     } else if (name == "bn32") {
       bn32_mode = value;
       drop_loop_graphs();

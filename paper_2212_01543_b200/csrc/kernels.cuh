@@ -532,7 +532,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 
 inline size_t attn_heads_smem(int d) { return (size_t)(32 + 2 * AH_KC) * (d + AH_PAD) * 2 + AH_KC * sizeof(float); }
 
-template <int HT>  // heads (compile-time: index math by shifts)
+template <int HT>  // heads per CTA (compile-time: index math by shifts); blockIdx.y = head group
 __global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
     const int2* __restrict__ items, const bf16* __restrict__ q, int q_stride, const bf16* __restrict__ k,
     const bf16* __restrict__ v, int kv_stride, bf16* __restrict__ out, int out_stride, const int* __restrict__ q_off,
@@ -551,6 +551,13 @@ __global__ void __launch_bounds__(512, 2) attn_prefill_heads_kernel(
   const int2 it = items[blockIdx.x];
   const int s = it.x, qbeg = it.y * 32;
   const int tid = threadIdx.x, nthr = blockDim.x;
+  {  // head group blockIdx.y: its d columns of q / k / v / out
+    const int hg = blockIdx.y * d;
+    q += hg;
+    k += hg;
+    v += hg;
+    out += hg;
+  }
   const int warp = tid >> 5, lane = tid & 31;
   const int qslot = q_slot[s], qlen = q_len[s];
   const int kvs = kv_map ? kv_map[s] : s;
