@@ -1948,6 +1948,7 @@ struct Engine : EngineBase {
       attn_head_groups = std::max(1, value);
     } else if (name == "fill") {
       fill_pct = std::max(1, std::min(100, value));
+      drop_loop_graphs();
     } else if (name == "bn32") {
       bn32_mode = value;
       drop_loop_graphs();
@@ -1989,10 +1990,13 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "ln_row") {
       ln_row = value;
+      drop_loop_graphs();
     } else if (name == "ln_row_min_tiles") {
       ln_row_min_tiles = value;
+      drop_loop_graphs();
     } else if (name == "res_red") {
       res_red = value != 0;
+      drop_loop_graphs();
     } else if (name == "ln_epi") {
       use_ln_epi = value != 0;
       drop_loop_graphs();
