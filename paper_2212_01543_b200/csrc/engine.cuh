@@ -719,12 +719,12 @@ struct Engine : EngineBase {
     return S;
   }
 
-  template <int BN, int ST, class Epi, int CL>
+  template <int BN, int ST, class Epi, int CL, bool PAIR = false>
   void tc_launch_cl(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi,
                     const int* M_dev) {
     if constexpr (BF16) {
-      auto kern = tc_gemm_kernel<BN, ST, Epi, CL>;
-      const int smem = TcSmem<BN, ST>::TOTAL;
+      auto kern = tc_gemm_kernel<BN, ST, Epi, CL, PAIR>;
+      const int smem = TcSmem<BN, ST, PAIR ? BN / 2 : BN>::TOTAL;
       smem_optin(kern, smem);
       const CUtensorMap& ta = tmap(A, a_cap, K, lda, TC_BM);
       const CUtensorMap& tb = tmap(W, N, K, K, BN / CL);
@@ -791,14 +791,23 @@ struct Engine : EngineBase {
   void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
     const int mt = cdiv(M, TC_BM);
     // wide-N GEMMs (vocabulary) pair up from 4 row tiles: their weight stream dominates L2 -> SM traffic
-    if (cluster_mode && (mt >= cluster_min_mtiles || (mt >= 4 && N >= 8192)) && choose_splits(M, N, K, BN) == 1)
+    if (cluster_mode && (mt >= cluster_min_mtiles || (mt >= 4 && N >= 8192)) && choose_splits(M, N, K, BN) == 1) {
+      // cta_group::2 pairs (option "pair"): half the weight tile per CTA, so more ring stages
+      if constexpr (BN >= 128) {
+        if (pair_mma) {
+          tc_launch_cl<BN, BN == 256 ? 6 : 8, Epi, 2, true>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+          return;
+        }
+      }
       tc_launch_cl<BN, ST, Epi, 2>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+    }
     else
       tc_launch_cl<BN, ST, Epi, 1>(A, a_cap, lda, M, W, N, K, epi, M_dev);
   }
 
   // widest N tile that still fills ~0.6 of the SMs (large-M encoder / Stage-II
   // GEMMs -> 256, Stage-I GEMMs with few row tiles -> 128 or 64)
+  int pair_mma = 0;  // option "pair": CTA-pair GEMMs as cta_group::2 MMAs instead of multicast weight tiles
   int bn32_mode = 1;  // option "bn32": 32-column tiles when 64-column tiles leave most SMs idle
   int fill_pct = 60;  // option "fill": SM share the widest tile must still reach
   int choose_bn(int M, int N) const {
@@ -1943,6 +1952,9 @@ struct Engine : EngineBase {
       use_graphs = value != 0;
     else if (name == "tail_ln") {
       use_tail_ln = value != 0;
+      drop_loop_graphs();
+    } else if (name == "pair") {
+      pair_mma = value;
       drop_loop_graphs();
     } else if (name == "attn_head_groups") {
       attn_head_groups = std::max(1, value);

@@ -25,10 +25,11 @@ constexpr int TC_EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half 
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr int TC_STG_LD = 32;  // epilogue transpose row pitch (floats); 16-byte slots XOR-swizzled by row
 
-template <int BN, int STAGES>
+// BROWS: weight rows staged per CTA (BN, or BN / 2 when a cta_group::2 pair splits them)
+template <int BN, int STAGES, int BROWS = BN>
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_BYTES = BROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFFSET = STAGES * STAGE_BYTES;                // epilogue staging
   static constexpr int STG_BYTES = TC_EPI_WARPS * 32 * TC_STG_LD * 4;
@@ -109,12 +110,21 @@ __device__ __forceinline__ void tc_load_b(uint8_t* dst, const CUtensorMap* tmB, 
 // operand traffic per tile drops from (128 + BN) to (128 + BN / 2) rows. A
 // stage is refilled only after both CTAs' MMAs released it (the empty
 // barrier counts one MMA-commit arrival from each CTA). Split-K is CL = 1 only.
-template <int BN, int STAGES, class Epi, int CL = 1>
+//
+// PAIR (CL = 2 only): the pair runs cta_group::2 MMAs instead -- one M = 256 x BN
+// instruction issued by the leader CTA reads A's 128 rows from each CTA and B's BN
+// rows as BN / 2 + BN / 2 from the two CTAs, so each CTA stages only half the weight
+// tile (no multicast) and its shared memory feeds half the B operand per MMA. Both
+// CTAs' TMA loads complete on the leader's full barrier; the leader's commits
+// multicast to both CTAs' empty / accumulator-full barriers; both CTAs' epilogue
+// warps release an accumulator on the leader's barrier.
+template <int BN, int STAGES, class Epi, int CL = 1, bool PAIR = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int M, int N, int K, const int* __restrict__ M_dev, Epi epi,
                    SplitK sk) {
-  using L = TcSmem<BN, STAGES>;
+  static_assert(!PAIR || CL == 2, "cta_group::2 needs a CTA pair");
+  using L = TcSmem<BN, STAGES, PAIR ? BN / 2 : BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
@@ -138,15 +148,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], PAIR ? 1 : CL);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], TC_EPI_WARPS);
+      mbar_init(&tempty[a], PAIR ? 2 * TC_EPI_WARPS : TC_EPI_WARPS);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   if constexpr (CL > 1)
     cluster_sync_all();  // the peer's barriers are initialised before any multicast reaches them
@@ -161,6 +174,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // m-tile 0 (which exists for any M >= 1) gets its first STAGES weight tiles
   // requested before the grid-dependency wait, overlapping the previous
   // kernel's tail (the A tiles follow after the wait into the same stages).
+  // PAIR: every stage's bytes (both CTAs') complete on the leader's full barrier
+  const uint32_t full_l = PAIR ? mapa_shared(smem_u32(full), 0) : 0u;
+  auto arm = [&](int st) {
+    if (!PAIR || crank == 0) mbar_arrive_expect_tx(&full[st], (PAIR ? 2 : 1) * L::STAGE_BYTES);
+  };
+  auto load_a = [&](int st, int k0, int m0) {
+    uint8_t* dst = smem + st * L::STAGE_BYTES;
+    if constexpr (PAIR) tma_load_2d_pair(dst, &tmA, full_l + 8u * st, k0, m0);
+    else tma_load_2d(dst, &tmA, &full[st], k0, m0);
+  };
+  auto load_b = [&](int st, int k0, int n0, uint64_t pol) {
+    uint8_t* dst = smem + st * L::STAGE_BYTES + L::A_BYTES;
+    if constexpr (PAIR) tma_load_2d_pair(dst, &tmB, full_l + 8u * st, k0, n0 + crank * (BN / 2), pol);
+    else tc_load_b<BN, CL>(dst, &tmB, &full[st], k0, n0, crank, pol);
+  };
   int pre = 0;
   if (warp == 0 && lane == 0 && cid < n_tiles * S) {
     const int tile = cid / S, ks = cid - tile * S;
@@ -168,8 +196,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     pre = min(STAGES, kb1 - kb0);
     const uint64_t pol = policy_evict_last();
     for (int s2 = 0; s2 < pre; ++s2) {
-      mbar_arrive_expect_tx(&full[s2], L::STAGE_BYTES);
-      tc_load_b<BN, CL>(smem + s2 * L::STAGE_BYTES + L::A_BYTES, &tmB, &full[s2], (kb0 + s2) * TC_BK, tile * BN, crank, pol);
+      arm(s2);
+      load_b(s2, (kb0 + s2) * TC_BK, tile * BN, pol);
     }
   }
   pdl_wait();
@@ -189,13 +217,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int kb0 = ks * num_kb / S, kb1 = (ks + 1) * num_kb / S;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * L::STAGE_BYTES;
           if (u == cid && kb - kb0 < pre) {  // weight tile already requested before the PDL wait
-            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
+            load_a(stage, kb * TC_BK, m0);
           } else {
-            mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, m0);
-            tc_load_b<BN, CL>(sa + L::A_BYTES, &tmB, &full[stage], kb * TC_BK, n0, crank, pol_w);
+            arm(stage);
+            load_a(stage, kb * TC_BK, m0);
+            load_b(stage, kb * TC_BK, n0, pol_w);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -208,15 +235,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // tensor are zero-filled by TMA) so every byte lands before the CTA may exit
       if (cid >= num_units) {
         const int kb0 = (cid % S) * num_kb / S;
-        for (int s2 = 0; s2 < pre; ++s2)
-          tma_load_2d(smem + s2 * L::STAGE_BYTES, &tmA, &full[s2], (kb0 + s2) * TC_BK, 0);
-        for (int s2 = 0; s2 < pre; ++s2) mbar_wait(&full[s2], 0);
+        for (int s2 = 0; s2 < pre; ++s2) load_a(s2, (kb0 + s2) * TC_BK, 0);
+        if (!PAIR || crank == 0)
+          for (int s2 = 0; s2 < pre; ++s2) mbar_wait(&full[s2], 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
+    if (lane == 0 && (!PAIR || crank == 0)) {
+      // ===== MMA issuer (PAIR: the leader CTA, M = 256 across the pair) =====
+      constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * TC_BM : TC_BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -234,10 +261,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
           const uint32_t sb = sa + L::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k)
-            tc_mma_f16(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
-                       ((kb - kb0) | k) != 0);
-          if constexpr (CL > 1)
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            if constexpr (PAIR)
+              tc_mma_f16_pair(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
+                              ((kb - kb0) | k) != 0);
+            else
+              tc_mma_f16(d_tmem, sdesc_kmajor_sw128(sa + k * 32), sdesc_kmajor_sw128(sb + k * 32), idesc,
+                         ((kb - kb0) | k) != 0);
+          }
+          if constexpr (PAIR)
+            tc_commit_pair_mc(&empty[stage], (uint16_t)3);  // the stage is free in both CTAs
+          else if constexpr (CL > 1)
             tc_commit_mc(&empty[stage], (1u << CL) - 1);  // release the stage in both CTAs (B halves are shared)
           else
             tc_commit(&empty[stage]);
@@ -246,7 +280,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if constexpr (PAIR)
+          tc_commit_pair_mc(&tfull[acc], (uint16_t)3);
+        else
+          tc_commit(&tfull[acc]);
       }
     }
   } else {
@@ -455,7 +492,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if constexpr (EpiTmaStore<Epi>::value) {
       if (lane == 0) bulk_wait_all();  // staged tiles fully written before the CTA retires
@@ -468,7 +508,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
