@@ -452,9 +452,12 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     bf16* vc = p.vc + (size_t)li * p.rcap * p.cap * DC_D;
     // ---- self-attention projections: q / k / v of head hh, dims half * 32 .. +32 ----
     dc_gemv<DC_D, 32, R, 96>(chunk(cb), ys, os);
+    DC_TS();
     dc_gemv<DC_D, 32, R, 96>(chunk(cb + 1), ys, os + 32);
     dc_gemv<DC_D, 32, R, 96>(chunk(cb + 2), ys, os + 64);
     __syncthreads();
+    DC_TS();
+    issue_upto(cb + 3 + DC_NSLOT);  // a slot is refilled as soon as every warp has consumed it
     {
       for (int idx = tid; idx < R * 96; idx += DC_THREADS) {
         const int r = idx / 96, jf = idx - r * 96, j = jf >> 5, f = jf & 31;
@@ -465,13 +468,19 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
         qs[(r * 3 + j) * 64 + half * 32 + f] = v;
         const uint32_t a = dc_mapa(qs + (r * 3 + j) * 64 + half * 32 + f, (uint32_t)(c ^ 1));
         asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-        if (j == 1) kc[((size_t)r * p.cap + t) * DC_D + hh * 64 + half * 32 + f] = __float2bfloat16_rn(v);
-        if (j == 2) vc[((size_t)r * p.cap + t) * DC_D + hh * 64 + half * 32 + f] = __float2bfloat16_rn(v);
       }
     }
+    DC_TS();
     cluster_sync_all();  // B1: the pair's q / k / v complete
     DC_TS();
-    issue_upto(cb + 3 + DC_NSLOT);
+    // the new key / value into the cache after B1 (global stores before a release barrier would
+    // hold it up; this step's attention takes slot t from shared memory, later steps from here)
+    for (int idx = tid; idx < R * 64; idx += DC_THREADS) {
+      const int r = idx >> 6, j = 1 + (idx >> 5 & 1), f = idx & 31;
+      bf16* dst = j == 1 ? kc : vc;
+      dst[((size_t)r * p.cap + t) * DC_D + hh * 64 + half * 32 + f] =
+          __float2bfloat16_rn(qs[(r * 3 + j) * 64 + half * 32 + f]);
+    }
     // ---- self-attention over slots 0..t: the pair splits the keys ----
     for (int r = 0; r < ((p.dbg & 2) ? 0 : R); ++r) {
       const int nk = t + 1, mid = (nk + 1) / 2;
@@ -496,6 +505,7 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     // ---- Wo + residual: x[32 c .. +32] ----
     dc_gemv<DC_D, 32, R>(chunk(cb + 3), cs, os);
     __syncthreads();
+    issue_upto(cb + 4 + DC_NSLOT);
     for (int idx = tid; idx < R * 32; idx += DC_THREADS) {
       const int r = idx >> 5, f = idx & 31, col = 32 * c + f;
       os[r * 32 + f] = xs[r * DC_D + col] + (os[r * 32 + f] + pr[96 + f]);
@@ -504,12 +514,12 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     bcast_f32(xs, DC_D, 32 * c, 32);
     cluster_sync_all();  // B3
     DC_TS();
-    issue_upto(cb + 4 + DC_NSLOT);
     dc_layernorm<R>(xs, ln2g, ln2b, ys);
     __syncthreads();
     // ---- cross-attention query: dims 32 c .. +32 = head hh, half ----
     dc_gemv<DC_D, 32, R>(chunk(cb + 4), ys, os);
     __syncthreads();
+    issue_upto(cb + 5 + DC_NSLOT);
     for (int idx = tid; idx < R * 32; idx += DC_THREADS) {
       const int r = idx >> 5, f = idx & 31;
       const float v = (os[r * 32 + f] + pr[128 + f]) * p.att_scale;
@@ -519,7 +529,6 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     }
     cluster_sync_all();  // B4
     DC_TS();
-    issue_upto(cb + 5 + DC_NSLOT);
     // ---- cross-attention over the sentence memory ----
     for (int r = 0; r < ((p.dbg & 2) ? 0 : R); ++r) {
       const int S = p.src_len[r], mid = (S + 1) / 2;
@@ -542,6 +551,7 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     // ---- Woc + residual ----
     dc_gemv<DC_D, 32, R>(chunk(cb + 5), cs, os);
     __syncthreads();
+    issue_upto(cb + 6 + DC_NSLOT);
     for (int idx = tid; idx < R * 32; idx += DC_THREADS) {
       const int r = idx >> 5, f = idx & 31, col = 32 * c + f;
       os[r * 32 + f] = xs[r * DC_D + col] + (os[r * 32 + f] + pr[160 + f]);
@@ -550,29 +560,29 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     bcast_f32(xs, DC_D, 32 * c, 32);
     cluster_sync_all();  // B6
     DC_TS();
-    issue_upto(cb + 6 + DC_NSLOT);
     dc_layernorm<R>(xs, ln3g, ln3b, ys);
     __syncthreads();
     // ---- W1 + ReLU: hidden[128 c .. +128] (four 32-row chunks) ----
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
       dc_gemv<DC_D, 32, R, 128>(chunk(cb + 6 + j), ys, os + 32 * j);
+      __syncthreads();
+      issue_upto(cb + 7 + j + DC_NSLOT);  // the W2 chunks stream in under W1
     }
-    __syncthreads();
     for (int idx = tid; idx < R * 128; idx += DC_THREADS) os[idx] = fmaxf(os[idx] + pr[192 + (idx & 127)], 0.f);
     __syncthreads();
     bcast_bf16(hs, DC_FF, 128 * c, 128);
     cluster_sync_all();  // B7
     DC_TS();
-    issue_upto(cb + 10 + DC_NSLOT);
     // ---- W2 + residual: x[32 c .. +32] over K = FF (four 8-row chunks) ----
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
       const bf16* wch = chunk(cb + 10 + j);
       DC_TS();
       dc_gemv<DC_FF, 8, R, 32>(wch, hs, wsb + 8 * j);
+      __syncthreads();
+      issue_upto(cb + 11 + j + DC_NSLOT);  // the next layer's chunks
     }
-    __syncthreads();
     DC_TS();
     for (int idx = tid; idx < R * 32; idx += DC_THREADS) {
       const int r = idx >> 5, f = idx & 31, col = 32 * c + f;
@@ -582,7 +592,6 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     bcast_f32(xs, DC_D, 32 * c, 32);
     cluster_sync_all();  // B8
     DC_TS();
-    issue_upto(cb + DC_CPL + DC_NSLOT);
     // next layer's LN1, or the final LayerNorm into the vocabulary operand
     dc_layernorm<R>(xs, lnng, lnnb, ys);
     __syncthreads();
@@ -593,7 +602,7 @@ __global__ void __cluster_dims__(DC_CN, 1, 1) __launch_bounds__(DC_THREADS, 1) d
     *reinterpret_cast<uint4*>(p.y + (size_t)r * DC_D + 32 * c + 8 * q8) =
         *reinterpret_cast<const uint4*>(ys + r * DC_D + 32 * c + 8 * q8);
   }
-  cluster_sync_all();  // no CTA leaves while a peer may still write into its shared memory
+  // (no closing cluster barrier: the last remote shared-memory writes were published by B8)
   DC_TS();
   if (trace && c == 0 && tid == 0 && t == 5) {
     printf("dc trace t=%d R=%d:", t, R);

@@ -1296,8 +1296,11 @@ __global__ void rowstats_from_logits_kernel(const float* __restrict__ logits, in
 // lane's online {max, sum} and best (value desc, id asc) are warp-reduced.
 // Same results as merge_row<KT>(parts, row, 1): identical max and order of
 // the rescaled sums per lane, identical tie rule.
+template <bool CG = false>
 __device__ __forceinline__ RowStat merge_row1(const VocabParts& parts, int row) {
   const int lane = threadIdx.x & 31;
+  // CG: the partials were written by other CTAs of the running grid (fused selection tail)
+  auto ldp = [](const auto* q) { return CG ? __ldcg(q) : *q; };
   const size_t base = (size_t)row * parts.ntiles;
   constexpr int MAXP = 8;  // tiles per lane held in registers (ntiles <= 256)
   float pm[MAXP], ps[MAXP], pv[MAXP];
@@ -1307,15 +1310,15 @@ __device__ __forceinline__ RowStat merge_row1(const VocabParts& parts, int row) 
     const int t = lane + 32 * i;
     const bool ok = t < parts.ntiles;
     const size_t o = base + (ok ? t : 0);
-    pm[i] = ok ? parts.mx[o] : -INFINITY;
-    ps[i] = ok ? parts.sum[o] : 0.f;
-    pv[i] = ok ? parts.val[o] : -INFINITY;
-    pi[i] = ok ? parts.id[o] : 0x7fffffff;
+    pm[i] = ok ? ldp(parts.mx + o) : -INFINITY;
+    ps[i] = ok ? ldp(parts.sum + o) : 0.f;
+    pv[i] = ok ? ldp(parts.val + o) : -INFINITY;
+    pi[i] = ok ? ldp(parts.id + o) : 0x7fffffff;
   }
   float m = -INFINITY;
 #pragma unroll
   for (int i = 0; i < MAXP; ++i) m = fmaxf(m, pm[i]);
-  for (int t = lane + 32 * MAXP; t < parts.ntiles; t += 32) m = fmaxf(m, parts.mx[base + t]);
+  for (int t = lane + 32 * MAXP; t < parts.ntiles; t += 32) m = fmaxf(m, ldp(parts.mx + base + t));
   m = warp_max(m);
   float sm = 0.f, bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -1328,10 +1331,10 @@ __device__ __forceinline__ RowStat merge_row1(const VocabParts& parts, int row) 
     }
   }
   for (int t = lane + 32 * MAXP; t < parts.ntiles; t += 32) {
-    const float tm = parts.mx[base + t];
-    if (tm != -INFINITY) sm += parts.sum[base + t] * ex2f((tm - m) * LOG2E);
-    const float v = parts.val[base + t];
-    const int id = parts.id[base + t];
+    const float tm = ldp(parts.mx + base + t);
+    if (tm != -INFINITY) sm += ldp(parts.sum + base + t) * ex2f((tm - m) * LOG2E);
+    const float v = ldp(parts.val + base + t);
+    const int id = ldp(parts.id + base + t);
     if (id != 0x7fffffff && better(v, id, bv, bi)) {
       bv = v;
       bi = id;
@@ -1627,24 +1630,13 @@ __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restri
   warp_embed_ln<T>(E, pe, g, b, scale, d, ids[row], p, x + (size_t)row * d, y + (size_t)row * d);
 }
 
-template <typename T, int KT>
-__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, int k, StepCtl* ctl) {
-  pdl_enter();
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// Selection of one row by one warp (decoding.py:102-150 at beam 1) and the
+// next step's embedding: shared by greedy_select_kernel and the fused
+// vocabulary + selection tail of gemv_vocab_kernel.
+template <typename T>
+__device__ __forceinline__ void greedy_select_row(const RowStat& rs, const GreedyState& st, int row, int t, int k,
+                                                  int done_v, StepCtl* ctl) {
   const int lane = threadIdx.x & 31;
-  // the row's partials, done flag and the step control are requested together
-  // (row clamped to the launch's host bound; rows past the live count exit below)
-  const int rr = min(row, R - 1);
-  StepCtl c{};
-  if (ctl) c = *ctl;
-  const int done_v = st.done[rr];
-  const RowStat rs = KT == 1 ? merge_row1(parts, rr) : merge_row<KT>(parts, rr, 1);
-  if (ctl) {
-    R = c.R;
-    t = c.t;
-    k = c.k;
-  }
-  if (row >= R) return;
   int tok;
   if (done_v) {
     tok = st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
@@ -1678,6 +1670,26 @@ __global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, in
                      st.x + (size_t)row * st.d, static_cast<T*>(st.y) + (size_t)row * st.d);
 }
 
+template <typename T, int KT>
+__global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, int t, int k, StepCtl* ctl) {
+  pdl_enter();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // the row's partials, done flag and the step control are requested together
+  // (row clamped to the launch's host bound; rows past the live count exit below)
+  const int rr = min(row, R - 1);
+  StepCtl c{};
+  if (ctl) c = *ctl;
+  const int done_v = st.done[rr];
+  const RowStat rs = KT == 1 ? merge_row1(parts, rr) : merge_row<KT>(parts, rr, 1);
+  if (ctl) {
+    R = c.R;
+    t = c.t;
+    k = c.k;
+  }
+  if (row >= R) return;
+  greedy_select_row<T>(rs, st, row, t, k, done_v, ctl);
+}
+
 // End of one graph-resident Stage-I step: advance the control block and
 // decide whether the WHILE node runs another step (decoding.py:102, :149).
 __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ alive,
@@ -1701,25 +1713,24 @@ __global__ void stage1_advance_kernel(StepCtl* ctl, const int* __restrict__ aliv
 // 1 + the last unfinished row below the cap-predicted one (rows are cap-sorted;
 // every row past it has finished) -- the batch shrinks with the finished tail
 // instead of with the caps. ctl->pad accumulates the rows computed (statistics).
-__global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive, const int* __restrict__ done) {
-  pdl_enter();
-  __shared__ int s_last;
-  const StepCtl c = *ctl;
+// (one block; c = the control block as it stands after this step's selection)
+__device__ __forceinline__ void stage1_advance_block(StepCtl* ctl, const StepCtl& c, const int* __restrict__ alive,
+                                                     const int* __restrict__ done, int* s_last) {
   const int t = c.t + 1;
   const bool more = c.finished < c.nrows && t < c.max_cap && alive[t] > 0;
   int R = more ? alive[t] : 0;
   if (done != nullptr && more) {  // (block-uniform branch)
     int last = 0;
     for (int r = threadIdx.x; r < R; r += blockDim.x)
-      if (!done[r]) last = r + 1;
+      if (!__ldcg(done + r)) last = r + 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
     if (blockDim.x > 32) {  // small buckets launch one warp: no block barrier on the step's critical path
-      if (threadIdx.x == 0) s_last = 0;
+      if (threadIdx.x == 0) *s_last = 0;
       __syncthreads();
-      if ((threadIdx.x & 31) == 0 && last > 0) atomicMax(&s_last, last);
+      if ((threadIdx.x & 31) == 0 && last > 0) atomicMax(s_last, last);
       __syncthreads();
-      last = s_last;
+      last = *s_last;
     }
     R = last;
   }
@@ -1733,6 +1744,58 @@ __global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict_
       ctl->pad = c.pad + R;
     }
   }
+}
+
+__global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict__ alive, const int* __restrict__ done) {
+  pdl_enter();
+  __shared__ int s_last;
+  const StepCtl c = *ctl;
+  stage1_advance_block(ctl, c, alive, done, &s_last);
+}
+
+// Fused tail of the Stage-I vocabulary GEMV (greedy, graph-resident loop): the
+// last CTA of the grid to finish its tile partials selects every live row's
+// token (greedy_select_row) and advances the control block
+// (stage1_advance_block), so a step is decoder -> vocabulary, two launches
+// fewer than decoder -> vocabulary -> selection -> advance.
+struct GvSelect {
+  unsigned* counter;  // arrival counter (zero before the launch; the last CTA resets it)
+  GreedyState st;
+  StepCtl* ctl;
+  const int* alive;
+};
+
+template <typename T>
+__device__ __forceinline__ void gv_select_tail(const VocabParts& parts, const GvSelect& sel) {
+  __shared__ int s_flag;
+  __threadfence();  // this CTA's partials before its arrival
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag = atomicAdd(sel.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  StepCtl* ctl = sel.ctl;
+  const int R = __ldcg(&ctl->R), t = __ldcg(&ctl->t), k = __ldcg(&ctl->k);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = warp; row < R; row += nw) {  // warp-uniform
+    const int done_v = __ldcg(sel.st.done + row);
+    const RowStat rs = merge_row1<true>(parts, row);
+    greedy_select_row<T>(rs, sel.st, row, t, k, done_v, ctl);
+  }
+  __threadfence();
+  __syncthreads();
+  StepCtl c;
+  c.t = t;
+  c.R = R;
+  c.k = k;
+  c.pos = __ldcg(&ctl->pos);
+  c.max_cap = __ldcg(&ctl->max_cap);
+  c.nrows = __ldcg(&ctl->nrows);
+  c.finished = atomicAdd(&ctl->finished, 0);
+  c.pad = __ldcg(&ctl->pad);
+  __shared__ int s_last;
+  stage1_advance_block(ctl, c, sel.alive, sel.st.done, &s_last);
+  if (threadIdx.x == 0) *sel.counter = 0;
 }
 
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.
