@@ -32,7 +32,6 @@
 #include "tc_gemm_ln.cuh"
 #include "tc_gemm_lnrow.cuh"
 #include "decode_cluster.cuh"
-#include "enc_cluster.cuh"
 #include "tmap.h"
 
 #include "engine_iface.h"
@@ -121,7 +120,6 @@ struct Engine : EngineBase {
   int *o_tokens, *o_lens, *o_calls;
   double* o_scores;
   unsigned char* o_forced;
-  unsigned* s_selcnt;  // arrival counter of the fused vocabulary + selection tail (zero between launches)
   int* h_meta = nullptr;  // pinned staging for per-call metadata (one H2D copy)
   StepCtl* h_ctl = nullptr;  // pinned copy of the loop control after a call (row statistics)
   bool unrolled_last = false;
@@ -627,7 +625,6 @@ struct Engine : EngineBase {
       o_calls = p.take<int>(base, Bmax);
       o_scores = p.take<double>(base, (size_t)Bmax * 3);
       o_forced = p.take<unsigned char>(base, Bmax);
-      s_selcnt = p.take<unsigned>(base, 8);
       return p.off;
     };
     size_t pbytes = persist_plan(nullptr);
@@ -1249,11 +1246,10 @@ struct Engine : EngineBase {
   // ln_g != nullptr: the rows are LN(s1.x) with the final decoder LayerNorm
   // (dec_lng / dec_lnb), computed in the GEMV prologue
   void vocab_parts(const T* y, int y_cap, int R, VocabParts& parts, int kt, int norm_allowed, float* logits_buf,
-                   const int* M_dev = nullptr, const float* ln_g = nullptr, const GvSelect* sel = nullptr) {
+                   const int* M_dev = nullptr, const float* ln_g = nullptr) {
     if (R <= 0) return;
     if constexpr (BF16) {
       if ((kt == 1 || (kt <= 5 && !ln_g)) && gemv_vocab_ok(R)) {
-        const GvSelect gsel = sel ? *sel : GvSelect{};
         parts.ntiles = cdiv(V, GV_VTILE);
         Scope sc(this, K_VOCAB | K_GEMM, 2.0 * ((double)V * d + (double)R * d), 2.0 * R * (double)V * d);
         const bf16* yb = reinterpret_cast<const bf16*>(y);
@@ -1263,15 +1259,11 @@ struct Engine : EngineBase {
 #define HRT_GVV(NT)                                                                                          \
   do {                                                                                                       \
     if (kt > 1)                                                                                              \
-      launch(gemv_vocab_kernel<NT, false, 5>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln, gsel); \
-    else if (ln_g && sel)                                                                                    \
-      launch(gemv_vocab_kernel<NT, true, 1, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln, gsel); \
+      launch(gemv_vocab_kernel<NT, false, 5>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
     else if (ln_g)                                                                                           \
-      launch(gemv_vocab_kernel<NT, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln, gsel); \
-    else if (sel)                                                                                            \
-      launch(gemv_vocab_kernel<NT, false, 1, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln, gsel); \
+      launch(gemv_vocab_kernel<NT, true>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
     else                                                                                                     \
-      launch(gemv_vocab_kernel<NT, false>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln, gsel); \
+      launch(gemv_vocab_kernel<NT, false>, grid, GV_VWARPS * 32, 0, yb, d, Eb, V, d, R, M_dev, parts, norm_allowed, ln); \
   } while (0)
         if (R <= 8)
           HRT_GVV(1);
@@ -1364,72 +1356,6 @@ struct Engine : EngineBase {
   // cross-K/V projection of every decoder layer (infer.py:216-220).
   // d_ids / d_pos hold the packed tokens; seq metadata in device arrays.
   // -------------------------------------------------------------------------
-  // encoder layers of <= 64 packed tokens as one 16-CTA cluster launch each (enc_cluster.cuh)
-  int enc_cluster_mode = 0;   // option "enc_cluster" (off: measured slower at every M, see DESIGN)
-  int enc_cluster_state = -1;  // -1 unknown, 0 unavailable on this device, 1 available
-  int ec_trace = 0;            // option "ec_trace" (timing attribution printout)
-  bool enc_cluster_ok(int M) {
-    if constexpr (!BF16) return false;
-    if (!enc_cluster_mode || d != EC_D || ff != EC_FF || H != EC_H || M < 1 || M > EC_MAXM || p_mem_target ||
-        enc_skip)
-      return false;
-    if (enc_cluster_state < 0) {
-      auto prep = [&](auto kern) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EcSmem::TOTAL) != cudaSuccess)
-          return false;
-        cudaLaunchConfig_t c = {};
-        c.gridDim = dim3(EC_CN);
-        c.blockDim = dim3(EC_THREADS);
-        c.dynamicSmemBytes = EcSmem::TOTAL;
-        int n = 0;
-        return cudaOccupancyMaxActiveClusters(&n, kern, &c) == cudaSuccess && n >= 1;
-      };
-      const bool ok = prep(enc_cluster_kernel<false>) && prep(enc_cluster_kernel<true>);
-      cudaGetLastError();
-      enc_cluster_state = ok ? 1 : 0;
-    }
-    return enc_cluster_state == 1;
-  }
-  void run_encoder_cluster(int M, int nseq, const int* off, const int* len) {
-    for (int i = 0; i < Le; ++i) {
-      const EncW& w = enc[i];
-      auto fb = [&](const T* q) { return reinterpret_cast<const bf16*>(frag_of(q)); };
-      EcParams ep{};
-      ep.wqkv = fb(w.wqkv);
-      ep.wo = fb(w.wo);
-      ep.w1 = fb(w.w1);
-      ep.w2 = fb(w.w2);
-      ep.bqkv = w.bqkv;
-      ep.bo = w.bo;
-      ep.b1 = w.b1;
-      ep.b2 = w.b2;
-      ep.ln2g = w.ln2g;
-      ep.ln2b = w.ln2b;
-      ep.lnng = i + 1 < Le ? enc[i + 1].ln1g : enc_lng;
-      ep.lnnb = i + 1 < Le ? enc[i + 1].ln1b : enc_lnb;
-      ep.x = eb.x;
-      ep.y = reinterpret_cast<bf16*>(eb.y);
-      ep.qkv = reinterpret_cast<bf16*>(eb.qkv);
-      ep.ctx = reinterpret_cast<bf16*>(eb.ctx);
-      ep.hid = reinterpret_cast<bf16*>(eb.hid);
-      ep.seq_off = off;
-      ep.seq_len = len;
-      ep.nseq = nseq;
-      ep.M = M;
-      ep.att_scale = att_scale;
-      ep.trace = ec_trace;
-      Tag _t(this, "encoder.cluster");
-      const double fl = 2.0 * M * (4.0 * d * d + 2.0 * d * ff);
-      Scope sc(this, K_GEMM | K_ATTN, 2.0 * (4.0 * d * d + 2.0 * d * ff), fl);
-      if (M > 32)
-        launch(enc_cluster_kernel<true>, EC_CN, EC_THREADS, EcSmem::TOTAL, ep);
-      else
-        launch(enc_cluster_kernel<false>, EC_CN, EC_THREADS, EcSmem::TOTAL, ep);
-      check_launch();
-    }
-  }
-
   void run_encoder(int M, int nseq, int max_len_seq, const int* off, const int* len, const int* items, int n_items) {
     Tag _tg(this, "encoder");
     if (M > Me_max) throw HrtError(HRT_ERR_MEMORY, "encoder tokens exceed max_src_tokens");
@@ -1437,11 +1363,6 @@ struct Engine : EngineBase {
       embed_ln(d_ids, d_pos, 0, M, enc[0].ln1g, enc[0].ln1b, eb.x, eb.y);
     else
       embed_ln(d_ids, d_pos, 0, M, enc_lng, enc_lnb, eb.x, eb.y);
-    if (Le > 0 && enc_cluster_ok(M)) {
-      run_encoder_cluster(M, nseq, off, len);
-      gemm(K_GEMM, eb.y, Me_max, d, M, wxkv, Ld * 2 * d, d, EpiBiasT<T, false>{xkv, Ld * 2 * d, bxkv});
-      return;
-    }
     const int sk = enc_skip;  // debug attribution: 1 LN, 2 attention, 4 projections (wrong results)
     for (int i = 0; i < Le; ++i) {
       const EncW& w = enc[i];
@@ -1901,13 +1822,8 @@ struct Engine : EngineBase {
   // One Stage-I step for R live rows (R is an upper bound when ctl != null):
   // decoder layers, vocab statistics, selection (greedy or beam), which also
   // embeds the next step's inputs.
-  // fuse_advance (plain loop graphs): the step may also advance the control block
-  // (returns true when it did: the vocabulary GEMV's last CTA selects and advances)
-  // option "sel_fuse" (off): measured slower at batch 1 (36.7 vs 35.0 us per step) -- the last
-  // CTA's serial merge + embed + advance costs more than the two PDL-chained launches it replaces
-  bool sel_fuse = false;
-  bool stage1_step(int R, int t, int k, int beam, int max_src, const int* src_off, const int* src_len,
-                   const GreedyState& gs, const BeamState& bs, StepCtl* ctl, bool fuse_advance = false) {
+  void stage1_step(int R, int t, int k, int beam, int max_src, const int* src_off, const int* src_len,
+                   const GreedyState& gs, const BeamState& bs, StepCtl* ctl) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     if (beam == 1) {
       const bool fuse = ln_fusable(R) && !(s1_skip & 1);  // final LN inside the vocab GEMV
@@ -1925,12 +1841,6 @@ struct Engine : EngineBase {
         throw;
       }
       greedy_hist_identity = false;
-      if (BF16 && fuse_advance && sel_fuse && ctl && gemv_vocab_ok(R) && !(s1_skip & 24)) {
-        Tag _tg(this, "s1.vocab");
-        const GvSelect sel{s_selcnt, gs, ctl, s_alive};
-        vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd, fuse ? dec_lng : nullptr, &sel);
-        return true;
-      }
       {
         Tag _tg(this, "s1.vocab");
         if (!(s1_skip & 8)) vocab_parts(s1.y, R_max, R, s1.parts, 1, 0, s1.logits, Rd, fuse ? dec_lng : nullptr);
@@ -1962,7 +1872,6 @@ struct Engine : EngineBase {
         check_launch();
       }
     }
-    return false;
   }
 
   // Capture (once per row bucket and beam width) the Stage-I step as the body
@@ -1978,11 +1887,10 @@ struct Engine : EngineBase {
     CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
     try {
       for (int u = 0; u < U; ++u) {
-        if (!stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl, true)) {
-          launch(stage1_advance_plain_kernel, 1, bucket <= 32 ? 32 : 256, 0, s_ctl, s_alive,
-                 beam == 1 ? (const int*)s_done : nullptr);
-          check_launch();
-        }
+        stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
+        launch(stage1_advance_plain_kernel, 1, bucket <= 32 ? 32 : 256, 0, s_ctl, s_alive,
+               beam == 1 ? (const int*)s_done : nullptr);
+        check_launch();
       }
     } catch (...) {
       cudaGraph_t dummy;
@@ -2052,13 +1960,6 @@ struct Engine : EngineBase {
       attn_head_groups = std::max(1, value);
     } else if (name == "fill") {
       fill_pct = std::max(1, std::min(100, value));
-      drop_loop_graphs();
-    } else if (name == "enc_cluster") {
-      enc_cluster_mode = value;
-    } else if (name == "ec_trace") {
-      ec_trace = value;
-    } else if (name == "sel_fuse") {
-      sel_fuse = value != 0;
       drop_loop_graphs();
     } else if (name == "bn32") {
       bn32_mode = value;

@@ -387,13 +387,11 @@ constexpr int GV_VTILE = GV_VWARPS * 16;
 // KT = 1: {max, sum, top-1} (greedy selection, Stage-II argmax); KT > 1 (beam search,
 // decoding.py:113 top-(b+1)): the tile's KT best allowed (value desc, id asc) per row,
 // picked by one thread per row from the 128 logits staged in shared memory.
-// SEL: the last CTA also selects the rows' tokens and advances the Stage-I loop
-// (gv_select_tail; greedy, graph-resident loop only).
-template <int NT, bool LNA = false, int KT = 1, bool SEL = false>
-__global__ void __launch_bounds__(GV_VWARPS * 32, LNA ? 1 : 2) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
+template <int NT, bool LNA = false, int KT = 1>
+__global__ void __launch_bounds__(GV_VWARPS * 32) gemv_vocab_kernel(const bf16* __restrict__ A, int lda,
                                                                 const bf16* __restrict__ E, int V, int K, int M,
                                                                 const int* __restrict__ M_dev, VocabParts parts,
-                                                                int norm_allowed, GvLN ln, GvSelect sel) {
+                                                                int norm_allowed, GvLN ln) {
   __shared__ float4 ws[GV_VWARPS][8 * NT];
   __shared__ float lg[KT > 1 ? 8 * NT : 1][KT > 1 ? GV_VTILE : 1];  // KT > 1: the tile's logits per row
   __shared__ float2 lnst[LNA ? 8 * NT : 1];
@@ -533,7 +531,6 @@ __global__ void __launch_bounds__(GV_VWARPS * 32, LNA ? 1 : 2) gemv_vocab_kernel
       }
     }
   }
-  if constexpr (SEL) gv_select_tail<bf16>(parts, sel);
 }
 
 }  // namespace hrt

@@ -1753,51 +1753,6 @@ __global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict_
   stage1_advance_block(ctl, c, alive, done, &s_last);
 }
 
-// Fused tail of the Stage-I vocabulary GEMV (greedy, graph-resident loop): the
-// last CTA of the grid to finish its tile partials selects every live row's
-// token (greedy_select_row) and advances the control block
-// (stage1_advance_block), so a step is decoder -> vocabulary, two launches
-// fewer than decoder -> vocabulary -> selection -> advance.
-struct GvSelect {
-  unsigned* counter;  // arrival counter (zero before the launch; the last CTA resets it)
-  GreedyState st;
-  StepCtl* ctl;
-  const int* alive;
-};
-
-template <typename T>
-__device__ __forceinline__ void gv_select_tail(const VocabParts& parts, const GvSelect& sel) {
-  __shared__ int s_flag;
-  __threadfence();  // this CTA's partials before its arrival
-  __syncthreads();
-  if (threadIdx.x == 0) s_flag = atomicAdd(sel.counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-  StepCtl* ctl = sel.ctl;
-  const int R = __ldcg(&ctl->R), t = __ldcg(&ctl->t), k = __ldcg(&ctl->k);
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int row = warp; row < R; row += nw) {  // warp-uniform
-    const int done_v = __ldcg(sel.st.done + row);
-    const RowStat rs = merge_row1<true>(parts, row);
-    greedy_select_row<T>(rs, sel.st, row, t, k, done_v, ctl);
-  }
-  __threadfence();
-  __syncthreads();
-  StepCtl c;
-  c.t = t;
-  c.R = R;
-  c.k = k;
-  c.pos = __ldcg(&ctl->pos);
-  c.max_cap = __ldcg(&ctl->max_cap);
-  c.nrows = __ldcg(&ctl->nrows);
-  c.finished = atomicAdd(&ctl->finished, 0);
-  c.pad = __ldcg(&ctl->pad);
-  __shared__ int s_last;
-  stage1_advance_block(ctl, c, sel.alive, sel.st.done, &s_last);
-  if (threadIdx.x == 0) *sel.counter = 0;
-}
-
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.
 template <int KT>
 __global__ void rowstat_kernel(VocabParts parts, int R, int kt, RowStat* __restrict__ out,

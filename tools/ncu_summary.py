@@ -54,7 +54,8 @@ def main():
     for k, (n, us, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"{k:34s} {n:8d} {us / 1000:9.3f} {100 * us / tot:5.1f}% {us / n:10.2f} {b / n / 1e6:15.3f}")
     if a.traffic_json:
-        gem = [d for d in per.values() if "tc_gemm_kernel" in d["name"]]
+        # every tcgen05 GEMM launch (plain + the fused residual + LayerNorm kernels), as bench.py's GEMM class
+        gem = [d for d in per.values() if "tc_gemm" in d["name"]]
         tb = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in gem)
         out = {"source": a.csv, "gemm_launches": len(gem), "gemm_dram_bytes_total": tb,
                "gemm_dram_bytes_per_launch": tb / max(1, len(gem)),

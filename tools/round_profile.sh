@@ -7,8 +7,8 @@ OUT=gpurun_out
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q > $OUT/${TAG}_pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1
-timeout 600 python bench.py > $OUT/${TAG}_bench.log 2>&1
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/${TAG}_bench_ref.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/${TAG}_bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/${TAG}_bench_ref.log 2>&1
 # launch lists (eager launches: one ncu record per kernel)
 for B in 1024 1; do
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
@@ -19,4 +19,8 @@ done
 timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
   -k regex:tc_gemm_kernel -s 2 -c 1 -o $OUT/${TAG}_gemm_full \
   python tools/profile_step.py --batch 1024 --no-graph > $OUT/${TAG}_ncu_full.log 2>&1
+# the fused residual + LayerNorm GEMM (encoder Wo / W2 at B = 1024)
+timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
+  -k regex:tc_gemm_resln_row -s 1 -c 1 -o $OUT/${TAG}_resln_full \
+  python tools/profile_step.py --batch 1024 --no-graph > $OUT/${TAG}_ncu_resln.log 2>&1
 echo done
