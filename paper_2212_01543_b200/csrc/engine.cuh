@@ -756,8 +756,17 @@ struct Engine : EngineBase {
   // larger than that would run its last clusters as a second wave. GPCs hold
   // different SM counts, so this can be below num_sms / CL.
   std::map<std::pair<const void*, int>, int> resident_cache;
+  // option "sm_cap": SMs a persistent tcgen05 grid may occupy (0 = all). Below the SM count,
+  // the remaining SMs stay free for the latency-bound Stage-I kernels of other engines
+  // (pipelined batches on other streams) while this engine's large GEMMs run.
+  int sm_cap = 0;
   template <class K>
   int resident_clusters(K kern, int smem, int CL) {
+    const int cap = sm_cap > 0 ? std::max(1, std::min(num_sms, sm_cap) / CL) : num_sms;
+    return std::min(cap, resident_clusters_all(kern, smem, CL));
+  }
+  template <class K>
+  int resident_clusters_all(K kern, int smem, int CL) {
     if (CL == 1) return num_sms;
     auto key = std::make_pair(reinterpret_cast<const void*>(kern), CL);
     auto it = resident_cache.find(key);
@@ -1822,8 +1831,11 @@ struct Engine : EngineBase {
   // One Stage-I step for R live rows (R is an upper bound when ctl != null):
   // decoder layers, vocab statistics, selection (greedy or beam), which also
   // embeds the next step's inputs.
-  void stage1_step(int R, int t, int k, int beam, int max_src, const int* src_off, const int* src_len,
-                   const GreedyState& gs, const BeamState& bs, StepCtl* ctl) {
+  // fuse_advance (plain loop graphs): a greedy bucket of <= 4 rows selects and advances the
+  // control block in one launch (greedy_select_advance_kernel); returns true when it did
+  bool sel_adv = true;  // option "sel_adv"
+  bool stage1_step(int R, int t, int k, int beam, int max_src, const int* src_off, const int* src_len,
+                   const GreedyState& gs, const BeamState& bs, StepCtl* ctl, bool fuse_advance = false) {
     const int* Rd = ctl ? &ctl->R : nullptr;
     if (beam == 1) {
       const bool fuse = ln_fusable(R) && !(s1_skip & 1);  // final LN inside the vocab GEMV
@@ -1847,6 +1859,11 @@ struct Engine : EngineBase {
       }
       Tag _tg(this, "s1.select");
       Scope sc(this, K_OTHER, 0, 0);
+      if (fuse_advance && sel_adv && ctl && R <= 4 && !(s1_skip & 16)) {
+        launch(greedy_select_advance_kernel<T>, 1, 128, 0, s1.parts, gs, R, ctl, (const int*)s_alive);
+        check_launch();
+        return true;
+      }
       if (!(s1_skip & 16)) {
         launch(greedy_select_kernel<T, 1>, cdiv(R, 4), 128, 0, s1.parts, gs, R, t, k, ctl);
         check_launch();
@@ -1872,6 +1889,7 @@ struct Engine : EngineBase {
         check_launch();
       }
     }
+    return false;
   }
 
   // Capture (once per row bucket and beam width) the Stage-I step as the body
@@ -1887,10 +1905,11 @@ struct Engine : EngineBase {
     CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
     try {
       for (int u = 0; u < U; ++u) {
-        stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl);
-        launch(stage1_advance_plain_kernel, 1, bucket <= 32 ? 32 : 256, 0, s_ctl, s_alive,
-               beam == 1 ? (const int*)s_done : nullptr);
-        check_launch();
+        if (!stage1_step(bucket, 0, 0, beam, Lmax, s_srcoff, s_srclen, gs, bs, s_ctl, true)) {
+          launch(stage1_advance_plain_kernel, 1, bucket <= 32 ? 32 : 256, 0, s_ctl, s_alive,
+                 beam == 1 ? (const int*)s_done : nullptr);
+          check_launch();
+        }
       }
     } catch (...) {
       cudaGraph_t dummy;
@@ -1960,6 +1979,12 @@ struct Engine : EngineBase {
       attn_head_groups = std::max(1, value);
     } else if (name == "fill") {
       fill_pct = std::max(1, std::min(100, value));
+      drop_loop_graphs();
+    } else if (name == "sel_adv") {
+      sel_adv = value != 0;
+      drop_loop_graphs();
+    } else if (name == "sm_cap") {
+      sm_cap = std::max(0, value);
       drop_loop_graphs();
     } else if (name == "bn32") {
       bn32_mode = value;

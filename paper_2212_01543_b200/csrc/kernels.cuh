@@ -1630,41 +1630,44 @@ __global__ void embed_ln_kernel(const int* __restrict__ ids, const int* __restri
   warp_embed_ln<T>(E, pe, g, b, scale, d, ids[row], p, x + (size_t)row * d, y + (size_t)row * d);
 }
 
-// Selection of one row by one warp (decoding.py:102-150 at beam 1) and the
-// next step's embedding: shared by greedy_select_kernel and the fused
-// vocabulary + selection tail of gemv_vocab_kernel.
-template <typename T>
-__device__ __forceinline__ void greedy_select_row(const RowStat& rs, const GreedyState& st, int row, int t, int k,
-                                                  int done_v, StepCtl* ctl) {
+// Selection of one row by one warp (decoding.py:102-150 at beam 1): the
+// row's token (warp-uniform), its score / anchor / finish bookkeeping; *fin =
+// the row finished at this step.
+__device__ __forceinline__ int greedy_pick_row(const RowStat& rs, const GreedyState& st, int row, int t, int done_v,
+                                               StepCtl* ctl, int* fin) {
   const int lane = threadIdx.x & 31;
-  int tok;
-  if (done_v) {
-    tok = st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
-  } else {
-    tok = 0;
-    if (lane == 0) {
-      const bool last = (t == st.caps[row] - 1);
-      int best = rs.id[0];
-      float bl = rs.val[0];
-      if (best == 0x7fffffff) {  // non-finite logits: finish the row rather than emit a bogus id
-        best = EOS_ID;
-        bl = rs.eos;
-      }
-      tok = last ? EOS_ID : best;
-      const float logit = last ? rs.eos : bl;
-      const float lp = (logit - rs.mx) - rs.lse;
-      st.score[row] += (double)lp;
-      st.anchors[(size_t)row * st.cap + t] = tok;
-      st.feed[row] = tok;
-      if (tok == EOS_ID) {
-        st.done[row] = 1;
-        st.nsteps[row] = t + 1;
-        st.forced[row] = last ? 1 : 0;
-        if (ctl) atomicAdd(&ctl->finished, 1);
-      }
+  *fin = 0;
+  if (done_v) return st.feed[row];  // finished rows keep feeding EOS (outputs ignored)
+  int tok = 0;
+  if (lane == 0) {
+    const bool last = (t == st.caps[row] - 1);
+    int best = rs.id[0];
+    float bl = rs.val[0];
+    if (best == 0x7fffffff) {  // non-finite logits: finish the row rather than emit a bogus id
+      best = EOS_ID;
+      bl = rs.eos;
     }
-    tok = __shfl_sync(0xffffffffu, tok, 0);
+    tok = last ? EOS_ID : best;
+    const float logit = last ? rs.eos : bl;
+    const float lp = (logit - rs.mx) - rs.lse;
+    st.score[row] += (double)lp;
+    st.anchors[(size_t)row * st.cap + t] = tok;
+    st.feed[row] = tok;
+    if (tok == EOS_ID) {
+      st.done[row] = 1;
+      st.nsteps[row] = t + 1;
+      st.forced[row] = last ? 1 : 0;
+      if (ctl) atomicAdd(&ctl->finished, 1);
+    }
   }
+  tok = __shfl_sync(0xffffffffu, tok, 0);
+  *fin = tok == EOS_ID;
+  return tok;
+}
+
+// ... and the next step's embedding x = E[tok] * sqrt(d) + PE[(t + 1) k], y = LN1(x)
+template <typename T>
+__device__ __forceinline__ void greedy_embed_row(const GreedyState& st, int row, int t, int k, int tok) {
   if (st.x != nullptr)
     warp_embed_ln<T>(static_cast<const T*>(st.E), st.pe, st.ln_g, st.ln_b, st.scale, st.d, tok, (t + 1) * k,
                      st.x + (size_t)row * st.d, static_cast<T*>(st.y) + (size_t)row * st.d);
@@ -1687,7 +1690,9 @@ __global__ void greedy_select_kernel(VocabParts parts, GreedyState st, int R, in
     k = c.k;
   }
   if (row >= R) return;
-  greedy_select_row<T>(rs, st, row, t, k, done_v, ctl);
+  int fin;
+  const int tok = greedy_pick_row(rs, st, row, t, done_v, ctl, &fin);
+  greedy_embed_row<T>(st, row, t, k, tok);
 }
 
 // End of one graph-resident Stage-I step: advance the control block and
@@ -1751,6 +1756,50 @@ __global__ void stage1_advance_plain_kernel(StepCtl* ctl, const int* __restrict_
   __shared__ int s_last;
   const StepCtl c = *ctl;
   stage1_advance_block(ctl, c, alive, done, &s_last);
+}
+
+// Single-CTA row buckets (<= 4 greedy rows, one warp per row, plain loop
+// graphs): the selection and the step advance in one launch. The CTA knows
+// every row's new done flag and the step's finishes itself, and alive[t + 1]
+// is requested with the partials, so the advance (stage1_advance_plain_kernel's
+// rule) costs no extra memory round trip; it is decided before the embedding.
+template <typename T>
+__global__ void greedy_select_advance_kernel(VocabParts parts, GreedyState st, int R, StepCtl* ctl,
+                                             const int* __restrict__ alive) {
+  pdl_enter();
+  __shared__ int s_done[4], s_fin[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rr = min(warp, R - 1);
+  const StepCtl c = *ctl;
+  const int done_v = st.done[rr];
+  const int al = alive[c.t + 1];  // (alive holds max_cap + 1 entries)
+  const RowStat rs = merge_row1(parts, rr);
+  int tok = 0, fin = 0;
+  const bool live = warp < c.R;
+  if (live) tok = greedy_pick_row(rs, st, warp, c.t, done_v, ctl, &fin);
+  if (lane == 0) {
+    s_done[warp] = (warp < R && !live) ? done_v : (live ? (done_v | fin) : 1);
+    s_fin[warp] = fin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int finished = c.finished;
+    for (int r = 0; r < 4; ++r) finished += s_fin[r];
+    const int t = c.t + 1;
+    const bool more = finished < c.nrows && t < c.max_cap && al > 0;
+    if (finished >= c.nrows) {
+      ctl->R = 0;
+    } else if (more) {
+      int last = 0;  // 1 + the last unfinished row below the cap-predicted count
+      for (int r = 0; r < min(al, 4); ++r)
+        if (!s_done[r]) last = r + 1;
+      ctl->t = t;
+      ctl->R = last;
+      ctl->pos = t * c.k;
+      ctl->pad = c.pad + last;
+    }
+  }
+  if (live) greedy_embed_row<T>(st, warp, c.t, c.k, tok);
 }
 
 // Final per-row stats (protocol face / Stage II): amax + renormalised logprob.

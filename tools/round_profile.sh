@@ -23,4 +23,14 @@ timeout 900 ncu --set full --import-source on --clock-control none --profile-fro
 timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
   -k regex:tc_gemm_resln_row -s 1 -c 1 -o $OUT/${TAG}_resln_full \
   python tools/profile_step.py --batch 1024 --no-graph > $OUT/${TAG}_ncu_resln.log 2>&1
+# summaries travel back; the full reports stay on the box (gpurun returns <= 64 MiB)
+for R in gemm_full resln_full; do
+  [ -f $OUT/${TAG}_$R.ncu-rep ] && python tools/ncu_full_summary.py $OUT/${TAG}_$R.ncu-rep > $OUT/${TAG}_${R}_summary.txt 2>&1
+  mkdir -p /tmp/ncu_reps && mv -f $OUT/${TAG}_$R.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+done
+for B in 1024 1; do
+  [ -f $OUT/${TAG}_launches_c2_b$B.csv ] && python tools/ncu_summary.py $OUT/${TAG}_launches_c2_b$B.csv \
+    $( [ $B = 1024 ] && echo --traffic-json $OUT/${TAG}_gemm_traffic_c2_b1024.json ) > $OUT/${TAG}_launches_c2_b$B.txt 2>&1
+done
+du -sh $OUT
 echo done
