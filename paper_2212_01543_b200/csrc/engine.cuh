@@ -2398,8 +2398,16 @@ void Engine<T>::translate(const int32_t* ids, const int32_t* lens, int B, int k,
       // n steps as U-step graphs, U = graph_unroll, graph_unroll / 2, ..., 1
       // (binary decomposition: at most log2(graph_unroll) + 1 graphs per bucket)
       int left = t1 - t0;
-      // capture every size of this bucket on first use (no capture inside later timed calls)
-      for (int U = graph_unroll; U >= 1; U >>= 1) plain_graph(bucket, beam, U, gs, bs);
+      // capture every size of every bucket up to this call's largest on first use, so a
+      // later call whose tail ends in a bucket this one never reached (few long sentences)
+      // does not capture inside a timed region
+      {
+        const int top = bucket_of(alive[0]);
+        for (int b = 1;; b = std::min(2 * b, top)) {
+          for (int U = graph_unroll; U >= 1; U >>= 1) plain_graph(b, beam, U, gs, bs);
+          if (b == top) break;
+        }
+      }
       for (int U = graph_unroll; U >= 1 && left > 0; U >>= 1) {
         if (left < U) continue;
         LoopGraph& lg = plain_graph(bucket, beam, U, gs, bs);
