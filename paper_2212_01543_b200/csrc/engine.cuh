@@ -737,7 +737,7 @@ struct Engine : EngineBase {
           Epi e2 = epi;
           e2.red = true;
           const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL);
-          const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
+          const int grid = grid_clusters(units, resident_clusters(kern, smem, CL)) * CL;
           launch_cluster = CL;
           launch(kern, grid, TC_THREADS, smem, ta, tb, tc, M, N, K, M_dev, e2, sk);
           launch_cluster = 1;
@@ -746,7 +746,7 @@ struct Engine : EngineBase {
       }
       // M: count, or upper bound with M_dev; CL = 2 works on vertical tile pairs
       const int units = cdiv(N, BN) * cdiv(cdiv(M, TC_BM), CL) * sk.splits;
-      const int grid = std::min(units, resident_clusters(kern, smem, CL)) * CL;
+      const int grid = grid_clusters(units, resident_clusters(kern, smem, CL)) * CL;
       launch_cluster = CL;
       launch(kern, grid, TC_THREADS, smem, ta, tb, tc, M, N, K, M_dev, epi, sk);
       launch_cluster = 1;
@@ -760,6 +760,15 @@ struct Engine : EngineBase {
   // the remaining SMs stay free for the latency-bound Stage-I kernels of other engines
   // (pipelined batches on other streams) while this engine's large GEMMs run.
   int sm_cap = 0;
+  // option "balance": a persistent grid of as many clusters as the rounds need (same
+  // number of rounds as the full grid, fewer idle SMs in the last one: they stay free
+  // for the other engines' kernels when batches pipeline)
+  bool balance = true;
+  int grid_clusters(int units, int maxc) const {
+    if (!balance || units <= maxc) return std::min(units, maxc);
+    const int rounds = cdiv(units, maxc);
+    return cdiv(units, rounds);
+  }
   template <class K>
   int resident_clusters(K kern, int smem, int CL) {
     const int cap = sm_cap > 0 ? std::max(1, std::min(num_sms, sm_cap) / CL) : num_sms;
@@ -938,7 +947,7 @@ struct Engine : EngineBase {
       auto key = std::make_tuple(static_cast<const void*>(ra.x), M);
       auto itx = tmaps_x.find(key);
       if (itx == tmaps_x.end()) itx = tmaps_x.emplace(key, make_tmap_f32_tile(ra.x, M, d, ra.ldx)).first;
-      const int grid = std::min(cdiv(cdiv(M, TC_BM), 2), resident_clusters(kern, smem, 2)) * 2;
+      const int grid = grid_clusters(cdiv(cdiv(M, TC_BM), 2), resident_clusters(kern, smem, 2)) * 2;
       launch_cluster = 2;
       launch(kern, grid, TC_THREADS, smem, ta, tb, itx->second, M, K, M_dev, ra);
       launch_cluster = 1;
@@ -1982,6 +1991,9 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "sel_adv") {
       sel_adv = value != 0;
+      drop_loop_graphs();
+    } else if (name == "balance") {
+      balance = value != 0;
       drop_loop_graphs();
     } else if (name == "sm_cap") {
       sm_cap = std::max(0, value);
