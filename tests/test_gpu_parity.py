@@ -581,6 +581,14 @@ def test_bf16_c2_shape_large_batch(hrt):
     b = eng.translate_batch(srcs, 2, max_steps=caps)
     for x, y in zip(a, b):
         assert x.tokens == y.tokens and x.score == y.score
+    # persistent grids sized to their rounds (option balance) vs the full grid: the units map
+    # to other CTAs, the arithmetic of every tile is unchanged, so the results are bit-identical
+    eng.set_option("cluster", 1)
+    eng.set_option("balance", 0)
+    bb = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("balance", 1)
+    for x, y in zip(a, bb):
+        assert x.tokens == y.tokens and x.score == y.score
     # residual + LayerNorm fused into the tcgen05 epilogue (cluster of d / 256 CTAs exchanging
     # row statistics over DSMEM): only the LN summation order differs from GEMM + LN kernel
     eng.set_option("cluster", 1)
