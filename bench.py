@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--sweep", default="", help="comma list of extra batch sizes to report")
     ap.add_argument("--streams", type=int, default=1, help="concurrent engines (CUDA streams) per GPU")
-    ap.add_argument("--pipeline", type=int, default=4,
+    ap.add_argument("--pipeline", type=int, default=5,
                     help="engines (CUDA streams) that consecutive batches are dealt to round-robin; the timed "
                          "region is the whole K-batch job (1: one batch at a time, L2 flushed between)")
     ap.add_argument("--corpus-streams", type=int, default=4, help="concurrent engines for the C5 corpus run")
@@ -85,6 +85,14 @@ def workload(args, rank, step):
     srcs = W.make_sources(args.batch, seed, spec["lengths"])
     caps = W.stage1_caps(srcs, k)
     return spec, k, srcs, caps
+
+
+def prepare(engs, rows, b_at):
+    """Setup (untimed): capture every greedy Stage-I loop graph up to `rows` rows now, so
+    no timed call captures one (engine option prepare_graphs)."""
+    if b_at == 1:
+        for e in engs:
+            e.set_option("prepare_graphs", int(rows))
 
 
 def apply_opts(args, engs):
@@ -641,6 +649,7 @@ def run_engine(args):
                        max_sentences=per, max_beam=b_at) for _ in range(S)]
     eng = engs[0]
     apply_opts(args, engs)
+    prepare(engs, per * b_at, b_at)
     del model
 
     batches = [workload(args, rank, s) for s in range(args.warmup + args.steps)]
@@ -770,10 +779,13 @@ def run_engine(args):
                                     else "float32", device=local, max_sentences=B, max_beam=b_at)
                          for _ in range(P - 1)]
         apply_opts(args, pengs)
+        prepare(pengs, B, b_at)
         pstreams = [stream] + [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local))
                                for e in pengs[1:]]
         pipe = Pipeline(torch, pengs, pstreams, batches, k, b_at, pin)
-        warm = list(range(args.warmup))
+        # W warm-up batches dealt like the timed ones; when W < P the remaining engines get
+        # one more untimed pass over the warm-up batches, so no engine starts cold in the timed region
+        warm = list(range(args.warmup)) + [i % max(1, args.warmup) for i in range(args.warmup, P)]
         timed = list(range(args.warmup, args.warmup + args.steps))
         pipe.device_run(warm)
         pipe.host_run(warm[:2])
@@ -901,6 +913,7 @@ def run_engine(args):
         cmodel = hrt.HRTModel.random(c5["shape"], c5["seed"])
         cengs = [hrt.Engine(cmodel, dtype="bfloat16", device=local, max_sentences=mx, max_beam=1, max_src_tokens=8192)
                  for _ in range(args.corpus_streams)]
+        prepare(cengs, mx, 1)
         del cmodel
         cstreams = [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local)) for e in cengs]
         corpus = corpus_block(args, torch, cengs, cstreams, rank, ws, local, k, pin)
@@ -1006,6 +1019,7 @@ def run_corpus_line(args):
     model = hrt.HRTModel.random(c5["shape"], c5["seed"])
     engs = [hrt.Engine(model, dtype="bfloat16", device=local, max_sentences=mx, max_beam=1, max_src_tokens=8192)
             for _ in range(args.corpus_streams)]
+    prepare(engs, mx, 1)
     del model
     streams = [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local)) for e in engs]
     pin = lambda shape, dt: torch.zeros(shape, dtype={np.int32: torch.int32, np.float64: torch.float64,  # noqa

@@ -1931,6 +1931,31 @@ struct Engine : EngineBase {
     CUDA_OK(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
     return lg;
   }
+  // Capture every greedy (beam 1, b_nat 1) Stage-I loop graph for row buckets up to `rows`
+  // without running them (option "prepare_graphs" = rows): a server or benchmark calls it at
+  // setup, so no translate call ever captures (the kernel parameters are fixed pointers, the
+  // same GreedyState / BeamState translate() builds, cross-attention prefetch on as in its loop)
+  void prepare_graphs(int rows) {
+    if (!(BF16 && use_graphs && timed_class == 0 && graph_unroll > 0) || rows < 1) return;
+    GreedyState gs{E, pe, dec[0].ln1g, dec[0].ln1b, s1.x, s1.y, emb_scale, d, s_feed, s_done, s_nsteps, s_forced,
+                   s_score, s_anchors, s_caps, cap_max};
+    BeamState bs = beam_state(1, 1);
+    int top = 1;
+    while (top < rows) top <<= 1;
+    top = std::min(top, R_max);
+    const bool pf = cross_prefetch;
+    cross_prefetch = true;
+    try {
+      for (int b = 1;; b = std::min(2 * b, top)) {
+        for (int U = graph_unroll; U >= 1; U >>= 1) plain_graph(b, 1, U, gs, bs);
+        if (b == top) break;
+      }
+    } catch (...) {
+      cross_prefetch = pf;
+      throw;
+    }
+    cross_prefetch = pf;
+  }
   LoopGraph& loop_graph(int bucket, int beam, const GreedyState& gs, const BeamState& bs) {
     // captured kernel parameters depend on the bucket, beam and b_nat (finished-store layout)
     LoopGraph& lg = loop_graphs[(bucket * 16 + beam) * 16 + bs.bnat];
@@ -1992,6 +2017,8 @@ struct Engine : EngineBase {
     } else if (name == "sel_adv") {
       sel_adv = value != 0;
       drop_loop_graphs();
+    } else if (name == "prepare_graphs") {
+      prepare_graphs(value);
     } else if (name == "balance") {
       balance = value != 0;
       drop_loop_graphs();
