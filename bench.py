@@ -87,6 +87,20 @@ def workload(args, rank, step):
     return spec, k, srcs, caps
 
 
+# Engines that share one GPU (the pipelined batches, the corpus streams) take the widest
+# GEMM tiles in Stage I: fewer CTAs per projection, so the SMs a latency-bound Stage-I GEMM
+# would barely use stay free for the other engines' kernels (pipelined C2: +3-4 %; one
+# batch at a time: -2.5 %, so the single-engine measurements keep the latency defaults).
+THROUGHPUT_OPTS = {"fill": 20, "bn32": 0}
+LATENCY_OPTS = {"fill": 60, "bn32": 1}  # the engine defaults
+
+
+def set_opts(engs, opts):
+    for e in engs:
+        for name, val in opts.items():
+            e.set_option(name, int(val))
+
+
 def prepare(engs, rows, b_at):
     """Setup (untimed): capture every greedy Stage-I loop graph up to `rows` rows now, so
     no timed call captures one (engine option prepare_graphs)."""
@@ -778,6 +792,7 @@ def run_engine(args):
         pengs = [eng] + [hrt.Engine(hrt.HRTModel.random(sh, spec["seed"]), dtype="bfloat16" if spec["dtype"] == "bf16"
                                     else "float32", device=local, max_sentences=B, max_beam=b_at)
                          for _ in range(P - 1)]
+        set_opts(pengs, THROUGHPUT_OPTS)
         apply_opts(args, pengs)
         prepare(pengs, B, b_at)
         pstreams = [stream] + [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local))
@@ -801,10 +816,16 @@ def run_engine(args):
         d2h //= args.steps
         pipe_info = {"engines": P, "mode": f"{args.steps} consecutive batches dealt round-robin to {P} engines (one "
                                            "CUDA stream each); timed region = the whole job; no L2 flush: every "
-                                           "batch's activations (> 1 GB) exceed the 126 MB L2"}
+                                           "batch's activations (> 1 GB) exceed the 126 MB L2",
+                     "engine_options": "throughput mode " + ",".join(f"{n}={v}" for n, v in THROUGHPUT_OPTS.items()) +
+                                       " (widest Stage-I GEMM tiles), Stage-I graphs captured at setup"}
         for e in pengs[1:]:
             e.close()
         del pipe, pengs
+        # engine 0 goes on alone (roofline pass, batch 1, AT baseline): latency defaults again
+        set_opts([eng], LATENCY_OPTS)
+        apply_opts(args, [eng])
+        prepare([eng], per * b_at, b_at)
     # ---- roofline pass (engine 0 alone on one length bucket): GEMM class ----
     rb = batches[args.warmup]
     c0 = chunks_of(rb[3], S)[0]
@@ -913,6 +934,8 @@ def run_engine(args):
         cmodel = hrt.HRTModel.random(c5["shape"], c5["seed"])
         cengs = [hrt.Engine(cmodel, dtype="bfloat16", device=local, max_sentences=mx, max_beam=1, max_src_tokens=8192)
                  for _ in range(args.corpus_streams)]
+        set_opts(cengs, THROUGHPUT_OPTS)
+        apply_opts(args, cengs)
         prepare(cengs, mx, 1)
         del cmodel
         cstreams = [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local)) for e in cengs]
@@ -1019,6 +1042,8 @@ def run_corpus_line(args):
     model = hrt.HRTModel.random(c5["shape"], c5["seed"])
     engs = [hrt.Engine(model, dtype="bfloat16", device=local, max_sentences=mx, max_beam=1, max_src_tokens=8192)
             for _ in range(args.corpus_streams)]
+    set_opts(engs, THROUGHPUT_OPTS)
+    apply_opts(args, engs)
     prepare(engs, mx, 1)
     del model
     streams = [torch.cuda.ExternalStream(e.stream, device=torch.device("cuda", local)) for e in engs]
