@@ -88,11 +88,12 @@ def workload(args, rank, step):
 
 
 # Engines that share one GPU (the pipelined batches, the corpus streams) take the widest
-# GEMM tiles in Stage I: fewer CTAs per projection, so the SMs a latency-bound Stage-I GEMM
-# would barely use stay free for the other engines' kernels (pipelined C2: +3-4 %; one
-# batch at a time: -2.5 %, so the single-engine measurements keep the latency defaults).
-THROUGHPUT_OPTS = {"fill": 20, "bn32": 0}
-LATENCY_OPTS = {"fill": 60, "bn32": 1}  # the engine defaults
+# GEMM tiles in Stage I and one CTA per row for the decode attention at every row count:
+# fewer, fuller CTAs per latency-bound Stage-I kernel, so the SMs they would barely use stay
+# free for the other engines' kernels (pipelined C2: +3-5 %; one batch at a time: -2.5 %,
+# so the single-engine measurements keep the latency defaults).
+THROUGHPUT_OPTS = {"fill": 20, "bn32": 0, "attn_rows": 2}
+LATENCY_OPTS = {"fill": 60, "bn32": 1, "attn_rows": 1}  # the engine defaults
 
 
 def set_opts(engs, opts):
