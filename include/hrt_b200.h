@@ -153,7 +153,13 @@ hrt_status hrt_at_translate_batch(hrt_engine* eng, const int32_t* ids, const int
  *                   launch (cta_group::2 CTA pairs, whole 512-column rows per CTA, TMA-staged
  *                   epilogue); 0: GEMM + LayerNorm kernel; 2 / 3: register-epilogue variants
  *   "res_red"       1 (default): residual GEMM epilogues as L2 reductions (same bits)
- *   "gemv", "gemv_max_m", "bn32", "attn_heads", "attn_rows", "splitk", "ln_fuse", "tail_ln",
+ *   "balance"       1 (default): persistent GEMM grids sized to the rounds they need (same bits)
+ *   "sel_adv"       1 (default): greedy buckets of <= 4 rows select and advance in one launch
+ *   "prepare_graphs" n: capture every greedy Stage-I loop graph for up to n rows now (setup call
+ *                   for servers / benchmarks, so no later call captures)
+ *   "fill", "bn32", "attn_rows": tile width / decode-attention choices; fill=20, bn32=0,
+ *                   attn_rows=2 is the throughput mode for several engines sharing one GPU
+ *   "gemv", "gemv_max_m", "attn_heads", "splitk", "ln_fuse", "tail_ln", "sm_cap",
  *   "l2_persist": kernel-path switches documented in DESIGN.md §4 / §7. */
 hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value);
 
