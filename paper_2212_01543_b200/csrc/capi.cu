@@ -1,6 +1,7 @@
 // C ABI of include/hrt_b200.h over the per-dtype engines.
 #include <cstring>
 #include <memory>
+#include <utility>
 
 #include "engine_iface.h"
 
@@ -14,12 +15,16 @@ struct hrt_engine {
   std::unique_ptr<EngineBase> impl;
 };
 
-static std::string g_last_error;
+// per host thread: engines driven from several threads (EnginePool) must not race on it
+static thread_local std::string g_last_error;
 
+// need_eng: the call operates on an engine, so a NULL handle is an argument error
+// (HRT_ERR_INVALID) rather than a dereference
 template <class Fn>
-static hrt_status guarded(hrt_engine* eng, Fn&& fn) {
+static hrt_status guarded(hrt_engine* eng, bool need_eng, Fn&& fn) {
   try {
-    if (eng) cudaSetDevice(eng->impl->device);
+    if (!eng && need_eng) throw HrtError(HRT_ERR_INVALID, "null engine");
+    if (eng) CUDA_OK(cudaSetDevice(eng->impl->device));
     fn();
     return HRT_OK;
   } catch (const HrtError& e) {
@@ -32,13 +37,17 @@ static hrt_status guarded(hrt_engine* eng, Fn&& fn) {
     return HRT_ERR_CUDA;
   }
 }
+template <class Fn>
+static hrt_status guarded(hrt_engine* eng, Fn&& fn) {
+  return guarded(eng, true, std::forward<Fn>(fn));
+}
 
 extern "C" {
 
 int64_t hrt_param_count(const hrt_config* cfg) { return engine_param_count(*cfg); }
 
 hrt_status hrt_create(const hrt_config* cfg, const float* params, int64_t n_params, int32_t device, hrt_engine** out) {
-  return guarded(nullptr, [&] {
+  return guarded(nullptr, /*need_eng=*/false, [&] {
     if (!cfg || !params || !out) throw HrtError(HRT_ERR_INVALID, "null argument");
     if (n_params != engine_param_count(*cfg))
       throw HrtError(HRT_ERR_INVALID, "n_params " + std::to_string(n_params) + " != expected " +
@@ -57,7 +66,7 @@ hrt_status hrt_create(const hrt_config* cfg, const float* params, int64_t n_para
 void hrt_destroy(hrt_engine* eng) { delete eng; }
 
 hrt_status hrt_estimate_arena(const hrt_config* cfg, int64_t* phase_bytes) {
-  return guarded(nullptr, [&] {
+  return guarded(nullptr, /*need_eng=*/false, [&] {
     if (!cfg || !phase_bytes) throw HrtError(HRT_ERR_INVALID, "null argument");
     if (cfg->dtype == HRT_DTYPE_F32)
       estimate_arena_f32(*cfg, phase_bytes);
@@ -135,6 +144,7 @@ hrt_status hrt_set_option(hrt_engine* eng, const char* name, int32_t value) {
 hrt_status hrt_phase_times(hrt_engine* eng, float* ms3) {
   return guarded(eng, [&] {
     EngineBase* e = eng->impl.get();
+    if (!ms3) throw HrtError(HRT_ERR_INVALID, "null argument");
     if (!e->phase_valid) throw HrtError(HRT_ERR_INVALID, "no fused call recorded yet");
     CUDA_OK(cudaEventSynchronize(e->phase_ev[3]));
     for (int i = 0; i < 3; ++i) CUDA_OK(cudaEventElapsedTime(&ms3[i], e->phase_ev[i], e->phase_ev[i + 1]));
@@ -183,7 +193,7 @@ hrt_status hrt_timing_report(hrt_engine* eng, char* buf, int64_t cap) {
            std::to_string(kv.second.flops) + "]";
     }
     s += "}";
-    if ((int64_t)s.size() + 1 > cap) throw HrtError(HRT_ERR_INVALID, "report buffer too small");
+    if (!buf || (int64_t)s.size() + 1 > cap) throw HrtError(HRT_ERR_INVALID, "report buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);
   });
 }

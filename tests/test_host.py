@@ -238,3 +238,19 @@ def test_teacher_forced_accounting_flags_real_mismatches():
         toks[j] = 50 if toks[j] != 50 else 51
         r = O.greedy_teacher_forced(orc, src, 2, toks, cap)
         assert r["bad"] + r["s1_ties"] + r["s2_ties"] >= 1
+
+
+def test_abi_rejects_null_engine_without_touching_cuda(lib_path):
+    """Every engine call given a NULL handle returns HRT_ERR_INVALID with a message
+    (no dereference, no CUDA call: runs on a host without a GPU)."""
+    import ctypes as C
+
+    lib = _lib.load(lib_path)
+    assert lib.hrt_synchronize(None) == _lib.HRT_ERR_INVALID
+    assert b"null engine" in lib.hrt_last_error(None)
+    assert lib.hrt_set_option(None, b"graph_unroll", 16) == _lib.HRT_ERR_INVALID
+    assert lib.hrt_reorder(None, None) == _lib.HRT_ERR_INVALID
+    assert lib.hrt_phase_times(None, None) == _lib.HRT_ERR_INVALID
+    assert lib.hrt_translate_batch(None, None, None, 0, 2, 1, 1, C.c_float(1.0), None, None, 0) == _lib.HRT_ERR_INVALID
+    assert lib.hrt_stream(None) is None
+    assert lib.hrt_get_stats(None, None) == _lib.HRT_ERR_INVALID
