@@ -143,12 +143,14 @@ hrt_status hrt_at_translate_batch(hrt_engine* eng, const int32_t* ids, const int
                                   float length_penalty, const int32_t* max_steps, const hrt_translate_out* out,
                                   int32_t io_on_device);
 
-/* Engine options (speed only; "graphs", "graph_unroll", "cluster" are bit-identical, the kernel-path
+/* Engine options (speed only; "graphs", "graph_unroll", "cluster", "cluster4" are bit-identical, the kernel-path
  * switches change the bf16 summation order):
  *   "graphs"        1 (default): Stage-I steps replayed from captured CUDA graphs; 0: launched step by step
  *   "graph_unroll"  steps per captured graph (power of two <= 32, default 16); 0: one conditional
  *                   WHILE-node graph per row bucket (the original design, measured slower)
  *   "cluster"       1 (default): large-M tcgen05 GEMMs as CTA pairs sharing the weight tile
+ *   "cluster4"      0 (default); 1: clusters of four CTAs sharing it, from "cluster4_min_mtiles"
+ *                   row tiles up (same bits; measured slower)
  *   "ln_row"        1 (default, d = 512, bf16): residual projection + following LayerNorm in one
  *                   launch (cta_group::2 CTA pairs, whole 512-column rows per CTA, TMA-staged
  *                   epilogue); 0: GEMM + LayerNorm kernel; 2 / 3: register-epilogue variants

@@ -805,10 +805,19 @@ struct Engine : EngineBase {
   // tiles to pair up (large-batch encoder / Stage II / vocabulary GEMMs)
   int cluster_mode = 1;  // option "cluster"
   int cluster_min_mtiles = 16;
+  // clusters of four CTAs sharing the weight tile (a quarter each, multicast): option
+  // "cluster4" (1 = on), from cluster4_min_mtiles row tiles up (8 for the vocabulary)
+  int cluster4 = 0;
+  int cluster4_min_mtiles = 32;
   template <int BN, int ST, class Epi>
   void tc_launch(const T* A, int a_cap, int lda, int M, const T* W, int N, int K, const Epi& epi, const int* M_dev) {
     const int mt = cdiv(M, TC_BM);
     // wide-N GEMMs (vocabulary) pair up from 4 row tiles: their weight stream dominates L2 -> SM traffic
+    if (cluster4 && !pair_mma && (mt >= cluster4_min_mtiles || (mt >= 8 && N >= 8192)) &&
+        choose_splits(M, N, K, BN) == 1) {
+      tc_launch_cl<BN, ST, Epi, 4>(A, a_cap, lda, M, W, N, K, epi, M_dev);
+      return;
+    }
     if (cluster_mode && (mt >= cluster_min_mtiles || (mt >= 4 && N >= 8192)) && choose_splits(M, N, K, BN) == 1) {
       // cta_group::2 pairs (option "pair"): half the weight tile per CTA, so more ring stages
       if constexpr (BN >= 128) {
@@ -2063,6 +2072,12 @@ struct Engine : EngineBase {
       drop_loop_graphs();
     } else if (name == "cluster_decode") {
       cluster_decode_mode = value;
+      drop_loop_graphs();
+    } else if (name == "cluster4") {
+      cluster4 = value;
+      drop_loop_graphs();
+    } else if (name == "cluster4_min_mtiles") {
+      cluster4_min_mtiles = std::max(1, value);
       drop_loop_graphs();
     } else if (name == "ln_row") {
       ln_row = value;

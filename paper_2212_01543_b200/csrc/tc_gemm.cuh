@@ -91,8 +91,8 @@ struct EpiPrefetch<E, decltype(void(E::kPrefetch))> {
   static constexpr bool value = E::kPrefetch;
 };
 
-// B (weight) tile load: whole BN-row box (CL = 1), or this CTA's BN/2-row
-// half multicast to both CTAs of the pair (CL = 2; the tensor map's box is BN/2 rows)
+// B (weight) tile load: whole BN-row box (CL = 1), or this CTA's BN/CL-row
+// slice multicast to every CTA of the cluster (CL = 2 / 4; the tensor map's box is BN/CL rows)
 template <int BN, int CL>
 __device__ __forceinline__ void tc_load_b(uint8_t* dst, const CUtensorMap* tmB, uint64_t* bar, int k0, int n0,
                                           int crank, uint64_t pol) {
@@ -110,6 +110,8 @@ __device__ __forceinline__ void tc_load_b(uint8_t* dst, const CUtensorMap* tmB, 
 // operand traffic per tile drops from (128 + BN) to (128 + BN / 2) rows. A
 // stage is refilled only after both CTAs' MMAs released it (the empty
 // barrier counts one MMA-commit arrival from each CTA). Split-K is CL = 1 only.
+// CL = 4 (option "cluster4"): the same with four vertically adjacent tiles per
+// cluster, each CTA loading a quarter of the weight tile: (128 + BN / 4) rows per tile.
 //
 // PAIR (CL = 2 only): the pair runs cta_group::2 MMAs instead -- one M = 256 x BN
 // instruction issued by the leader CTA reads A's 128 rows from each CTA and B's BN
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  static_assert(CL == 1 || CL == 2, "cluster size");
+  static_assert(CL == 1 || CL == 2 || CL == 4, "cluster size");
   pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;

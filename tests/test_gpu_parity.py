@@ -589,6 +589,16 @@ def test_bf16_c2_shape_large_batch(hrt):
     eng.set_option("balance", 1)
     for x, y in zip(a, bb):
         assert x.tokens == y.tokens and x.score == y.score
+    # clusters of four CTAs sharing each weight tile (a quarter each, multicast), down to
+    # 4-row-tile GEMMs so Stage-I / Stage-II / vocabulary launches take them too: same tiles,
+    # same MMA order, bit-identical
+    eng.set_option("cluster4", 1)
+    eng.set_option("cluster4_min_mtiles", 4)
+    c4 = eng.translate_batch(srcs, 2, max_steps=caps)
+    eng.set_option("cluster4", 0)
+    eng.set_option("cluster4_min_mtiles", 32)
+    for x, y in zip(a, c4):
+        assert x.tokens == y.tokens and x.score == y.score
     # residual + LayerNorm fused into the tcgen05 epilogue (cluster of d / 256 CTAs exchanging
     # row statistics over DSMEM): only the LN summation order differs from GEMM + LN kernel
     eng.set_option("cluster", 1)

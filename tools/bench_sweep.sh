@@ -6,5 +6,7 @@ for v in "$@"; do
     --engine-opt "$v" 2>/dev/null | python -c "
 import json, sys
 l = [x for x in sys.stdin if x.startswith('{')][-1]; d = json.loads(l)
-print(f'{sys.argv[1]:28s} {d[\"value\"] / 1e6:.3f} M w/s  {d[\"ms_per_step\"]:.3f} ms/batch  e2e {d[\"e2e\"][\"value\"] / 1e6:.3f} M', flush=True)" "$v"
+u = d.get('unpipelined') or {}; ph = d.get('phase_ms_per_step') or {}
+print(f'{sys.argv[1]:28s} {d[\"value\"] / 1e6:.3f} M w/s  {d[\"ms_per_step\"]:.3f} ms/batch  e2e {d[\"e2e\"][\"value\"] / 1e6:.3f} M'
+      f'  | one batch at a time {u.get(\"value\", 0) / 1e6:.3f} M  enc {ph.get(\"encoder\", 0):.3f} s1 {ph.get(\"stage1\", 0):.3f} s2 {ph.get(\"stage2\", 0):.3f} ms', flush=True)" "$v"
 done
