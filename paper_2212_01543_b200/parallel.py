@@ -100,21 +100,25 @@ def gather_outputs(index, lens, tokens, group=None, device=None):
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = device if device is not None else torch.device("cpu")
-    n = torch.tensor([len(index)], dtype=torch.int64, device=dev)
+    tokens = np.asarray(tokens)
+    # row count and token width per rank (a rank with no sentences may hold an empty array,
+    # and ranks may size their output rows differently): every rank pads to the maxima
+    L_loc = tokens.shape[1] if tokens.ndim == 2 else 0
+    n = torch.tensor([len(index), L_loc], dtype=torch.int64, device=dev)
     ns = [torch.zeros_like(n) for _ in range(ws)]
     dist.all_gather(ns, n, group=group)
-    nmax = int(max(int(x.item()) for x in ns))
-    L = tokens.shape[1] if len(tokens.shape) == 2 else 0
+    nmax = int(max(int(x[0].item()) for x in ns))
+    L = int(max(int(x[1].item()) for x in ns))
     pack = torch.zeros((nmax, 2 + L), dtype=torch.int64, device=dev)
     if len(index):
         pack[: len(index), 0] = torch.as_tensor(np.asarray(index, np.int64), device=dev)
         pack[: len(index), 1] = torch.as_tensor(np.asarray(lens, np.int64), device=dev)
-        pack[: len(index), 2:] = torch.as_tensor(np.asarray(tokens, np.int64), device=dev)
+        pack[: len(index), 2:2 + L_loc] = torch.as_tensor(tokens.astype(np.int64), device=dev)
     parts = [torch.zeros_like(pack) for _ in range(ws)]
     dist.all_gather(parts, pack, group=group)
     if rank != 0:
         return None
-    rows = [p[: int(c.item())].cpu().numpy() for p, c in zip(parts, ns)]
+    rows = [p[: int(c[0].item())].cpu().numpy() for p, c in zip(parts, ns)]
     allr = np.concatenate(rows) if rows else np.zeros((0, 2 + L), np.int64)
     return allr[:, 0], allr[:, 1].astype(np.int32), allr[:, 2:].astype(np.int32)
 

@@ -94,3 +94,39 @@ def test_gloo_world2_gather_and_reductions():
         assert olen[i] == len(o) and toks[i][: len(o)] == o
     assert tmax == 2.0
     assert wsum == float(sum(olen))
+
+
+def _worker_ragged(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if rank == 0:  # three sentences, 8-wide output rows
+        idx = np.array([5, 1, 3], np.int64)
+        olen = np.array([2, 8, 0], np.int32)
+        toks = np.arange(24, dtype=np.int32).reshape(3, 8)
+    else:  # no bucket on this rank: empty arrays of any shape
+        idx, olen, toks = np.zeros(0, np.int64), np.zeros(0, np.int32), np.zeros(0, np.int32)
+    got = P.gather_outputs(idx, olen, toks)
+    if rank == 0:
+        q.put((got[0].tolist(), got[1].tolist(), got[2].tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_gather_with_an_empty_rank():
+    """A rank without sentences (more ranks than buckets) passes empty arrays: the
+    gather agrees on row count and token width across ranks instead of failing."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ragged, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    idx, olen, toks = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert idx == [5, 1, 3] and olen == [2, 8, 0]
+    assert toks == np.arange(24).reshape(3, 8).tolist()
